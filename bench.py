@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: forward volume ray marching at 1080p on 1M Gaussians
+(BASELINE.json metric "Mrays/s & FPS forward at 1080p, 1M Gaussians"; config C3:
+Mip-NeRF360-shaped synthetic scene, adaptive sampling + empty-space skipping).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One JSON line on rank 0.  A "step" renders one full 1920x1080 frame (N>1: each
+rank renders the 16x16 tiles t = rank + k*N, then the tiles are gathered).
+`value` is device-timed (CUDA events on the render stream, L2 flushed before
+every step, max over ranks); `e2e` is the same metric through the public API
+with the camera passed from the host and the frame read back to pinned host
+memory inside the timed region.  `--impl reference` times the reference
+algorithm's CPU implementation (the float64 C port in oracle/, all host
+threads) on a bounded sample of the same frame.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mrays/s forward at 1080p, 1M Gaussians"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- workloads
+def workload(name: str):
+    """(records f32-representable [N,87], sigma_eps, camera kwargs, RenderConfig kwargs, desc)"""
+    from paper_2509_07782_b200.scenes import f32_records, gen_test_scene_records, synth_records
+
+    if name == "c1":
+        rec = f32_records(gen_test_scene_records("random-cloud", 10_000, seed=0, anisotropy=3.0,
+                                                 base_scale=0.01177))
+        cam = dict(radius=3.0, focal=64.0, width=64, height=64)
+        return rec, 0.01, cam, dict(mode="uniform"), "C1 10k random-cloud aniso 3, 64x64 uniform+ESS"
+    if name == "c3":
+        rec = synth_records("ball", 1_000_000, seed=0, anisotropy=3.0, r_max_bound=10.0,
+                            shell_fraction=0.3, shell_radius=(10.0, 50.0))
+        cam = dict(radius=3.5, focal=1.2 * 1920, width=1920, height=1080)
+        desc = ("C3 1M Gaussians: 70% ball r=1 + 30% background shell r=10-50 (scale ~ r), "
+                "anisotropy<=3 under r0=10 volume-ratio bound, 1920x1080, adaptive+ESS")
+        return rec, 0.01, cam, dict(mode="adaptive"), desc
+    raise ValueError(name)
+
+
+def make_camera(G, cam):
+    return G.orbit_cameras(1, radius=cam["radius"], focal=cam["focal"], width=cam["width"],
+                           height=cam["height"])[0]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._p = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self._p:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=2)
+            except Exception:
+                self._p.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU leg
+def cpu_rays(cam_kw, stride: int, offset: int = 0):
+    import oracle as O
+    import paper_2509_07782_b200.scenes as S
+
+    center, quat = S.orbit_poses(1, cam_kw["radius"])[0]
+    rays = O.camera_rays(center, quat, cam_kw["focal"], cam_kw["width"], cam_kw["height"])
+    rays = rays.reshape(cam_kw["height"], cam_kw["width"], 8)
+    oy, ox = divmod(offset, stride)
+    return rays[oy % stride::stride, ox::stride].reshape(-1, 8)
+
+
+def cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s: float = 15.0, steps: int = 1,
+                 offset0: int = 0):
+    """The reference algorithm's CPU implementation (oracle/, float64 C port of
+    renderer.py) on all host threads, on a stratified ray sample."""
+    import oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.time()
+    osc = O.OracleScene(rec, eps)
+    osc.reorder_by_morton()
+    build_s = time.time() - t0
+    cfg = O.OCfg.make(**cfg_kw)
+    # calibrate the sample size on a sparse probe
+    stride = 256
+    probe = cpu_rays(cam_kw, stride)
+    t0 = time.time()
+    osc.march_rays(probe, cfg, clip=True, threads=threads)
+    dt = max(time.time() - t0, 1e-3)
+    per_ray = dt / len(probe)
+    want = target_s / max(steps, 1) / per_ray
+    total = cam_kw["width"] * cam_kw["height"]
+    stride = int(max(2, min(256, math.floor(math.sqrt(total / max(want, 1.0))))))
+    times, nrays = [], 0
+    for k in range(steps):
+        rays = cpu_rays(cam_kw, stride, offset0 + k)
+        t0 = time.time()
+        osc.march_rays(rays, cfg, clip=True, threads=threads)
+        times.append(time.time() - t0)
+        nrays += len(rays)
+    value = nrays / sum(times) / 1e6
+    return {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "port",
+            "sample": f"every {stride}th pixel per axis of the frame ({nrays // max(steps, 1)} rays/step, "
+                      f"{steps} step(s), {sum(times):.1f} s); oracle scene prep+BVH {build_s:.1f} s",
+            "seconds": sum(times)}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    rec, eps, cam_kw, cfg_kw, desc = workload(args.config)
+    H, W = cam_kw["height"], cam_kw["width"]
+    config = {"workload": desc, "n_gaussians": int(rec.shape[0]), "width": W, "height": H,
+              "mode": cfg_kw.get("mode", "uniform"), "ess": True, "parallelism": f"tiles{world}",
+              "l2": "flushed (256 MiB write) before every timed step", "data": "synthetic"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=min(args.cpu_seconds * 2, 60.0),
+                          steps=args.steps + args.warmup)
+        v = cb["value"]
+        print(json.dumps({
+            "metric": METRIC, "value": v, "unit": "Mrays/s", "impl": "reference",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * H * W / (v * 1e6), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config, "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind",
+                                                                  "sample")},
+            "e2e": {"value": v, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2509_07782_b200 as G
+    from paper_2509_07782_b200 import _lib
+
+    dev = torch.device("cuda", local_rank)
+    cam = make_camera(G, cam_kw)
+    cfg = G.RenderConfig(**cfg_kw)
+
+    # ---- scene upload + build (K1-K5) + Morton reorder
+    params_host = torch.from_numpy(rec.astype(np.float32)).pin_memory()
+    t0 = time.time()
+    scene = G.Scene.from_records(params_host.to(dev))
+    G.reorder_by_morton(scene)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    # timed rebuild (K1 prepare + K2 morton + K3 sort + K5 LBVH), device events
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        scene._rebuild(validate=False)
+    e0.record(s)
+    for _ in range(5):
+        scene._rebuild(validate=False)
+    e1.record(s)
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1) / 5
+
+    # ---- algorithmic work counters (untimed stats pass)
+    rgb, depth, trans, st = G.render(scene, cam, cfg, stats=True)
+    torch.cuda.synchronize()
+    cnt = st.cpu().numpy().astype(np.float64)
+    keys = ["rays", "samples", "segments", "segments_skipped", "closest_hit_calls", "node_visits",
+            "aabb_hits", "ellipsoid_hits", "pairs", "composited"]
+    counters = dict(zip(keys, cnt.tolist()))
+    # FLOPs/ray = 33 P + 15 S + 165 Cr + 12 V
+    flops_frame = (33 * counters["pairs"] + 15 * counters["samples"] +
+                   165 * counters["ellipsoid_hits"] + 12 * counters["node_visits"])
+
+    # ---- FP32 roofline denominator: measured FFMA issue rate
+    sink = torch.empty(148 * 8 * 256 * 2, dtype=torch.float32, device=dev)
+    import ctypes
+
+    fl = ctypes.c_double(0)
+    L = _lib.lib()
+    L.gsx_calibrate_fp32(2000, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    e0.record(s)
+    L.gsx_calibrate_fp32(20000, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
+    e1.record(s)
+    torch.cuda.synchronize()
+    fp32_peak = fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+    # ---- timed forward
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    rgb = torch.zeros((H, W, 3), device=dev)
+    depth = torch.zeros((H, W), device=dev)
+    trans = torch.zeros((H, W), device=dev)
+    tb, ts = (rank, world) if world > 1 else (0, 1)
+
+    def step():
+        G.render(scene, cam, cfg, tile_begin=tb, tile_stride=ts, rgb=rgb, depth=depth,
+                 trans=trans)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(s)
+            step()
+            ends[k].record(s)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms = tot_ms / args.steps
+    mrays = H * W / (ms * 1e-3) / 1e6
+
+    # ---- e2e through the public API: camera from host, frame back to pinned host
+    host_rgb = torch.empty((H, W, 3), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        step()
+        host_rgb.copy_(rgb, non_blocking=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(args.steps):
+        flush.zero_()
+        step()
+        host_rgb.copy_(rgb, non_blocking=True)
+    e1.record(s)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps  # includes the L2 flush (conservative)
+    e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e6, "unit": "Mrays/s",
+           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": H * W * 3 * 4,
+           "note": "camera passed by value in the launch parameters; includes a 256 MiB L2 flush"}
+
+    if rank != 0:
+        return
+    achieved = flops_frame / (ms * 1e-3) / 1e12
+    roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak, "traffic": None,
+            "peak_source": "measured FFMA loop (gsx_calibrate_fp32) in this run",
+            "flops_per_frame": flops_frame,
+            "flops_model": "33*pairs + 15*samples + 165*ellipsoid_hits + 12*node_visits (SURVEY 8(d))"}
+    out = {
+        "metric": METRIC, "value": mrays, "unit": "Mrays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "fps": 1e3 / ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config, "roofline": roof, "e2e": e2e,
+        "gpu_launches": args.steps, "clocks": clk.summary(),
+        "build_ms": build_ms, "setup_s": setup_s,
+        "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
+        "step_ms": step_ms,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,1 +1,35 @@
-"""B200-native RayGaussX volumetric ray marcher (drop-in for gsray render path)."""
+"""B200-native RayGaussX volumetric ray marcher: a drop-in for the render path
+of the reference package `gsray` (/root/reference/pkg/src/gsray/__init__.py).
+
+Same entry-point names and layouts; the work runs in hand-written sm_100a
+kernels (libgsx.so, C ABI in include/gsx.h).  There is no CPU fallback.
+"""
+
+from .config import Camera, Ray, RenderConfig, RenderStats, quat_to_rotation, segment_step
+from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptyScene, GsrayError,
+                     ParseError, ValidationError)
+from .renderer import (clip_ray_to_scene, march_ray, march_rays, psnr, render, render_full,
+                       render_image)
+from .scene import Scene, gen_test_scene, load_scene, reorder_by_morton, save_scene
+from .scenes import orbit_poses, look_at
+
+
+def orbit_cameras(n, radius, focal, width, height, elevation=0.35, target=(0.0, 0.0, 0.0)):
+    """scene_io.py:175-187."""
+    return [Camera(center=c, quat=q, focal=focal, width=width, height=height)
+            for c, q in orbit_poses(n, radius, elevation, target)]
+
+
+def look_at_camera(center, target, focal, width, height, up=(0.0, 1.0, 0.0), **kw):
+    """scene_io.py:158-172."""
+    c, q = look_at(center, target, up)
+    return Camera(center=c, quat=q, focal=focal, width=width, height=height, **kw)
+
+
+__all__ = [
+    "BufferOverflow", "Camera", "DegenerateCenter", "EmptyIsosurface", "EmptyScene",
+    "GsrayError", "ParseError", "Ray", "RenderConfig", "RenderStats", "Scene",
+    "ValidationError", "clip_ray_to_scene", "gen_test_scene", "load_scene", "look_at_camera",
+    "march_ray", "march_rays", "orbit_cameras", "psnr", "quat_to_rotation", "render",
+    "render_full", "render_image", "reorder_by_morton", "save_scene", "segment_step",
+]

@@ -1,0 +1,185 @@
+"""Configuration and value types mirroring the reference renderer's
+(renderer.py:27-145): same field names, defaults and validation errors."""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import CameraC, RenderCfg
+
+
+@dataclass(frozen=True)
+class RenderConfig:
+    """renderer.py:27-49.  `tile_size` and `buffer_capacity` are accepted for
+    signature compatibility: pixels are tile-size invariant and overflow
+    splitting is bitwise neutral in the reference (renderer.py:361-371), so the
+    GPU path processes candidates in unbounded streams instead."""
+
+    dt: float = 0.0025
+    n_s: int = 16
+    t_eps: float = 1e-4
+    mode: str = "uniform"
+    beta: float = 1024.0
+    dt_min: float = 0.005
+    dt_max: float = 0.02
+    ess: bool = True
+    tile_size: int = 16
+    background: tuple = (0.0, 0.0, 0.0)
+    buffer_capacity: int = 64
+
+    def __post_init__(self):
+        if not (0.0 < self.t_eps < 1.0):
+            raise ValueError("t_eps must be in (0, 1)")
+        if self.n_s < 1:
+            raise ValueError("n_s must be >= 1")
+        if self.dt_min > self.dt_max:
+            raise ValueError("dt_min must be <= dt_max")
+        if self.mode not in ("uniform", "adaptive"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+
+    def to_c(self) -> RenderCfg:
+        c = RenderCfg()
+        c.dt, c.n_s, c.t_eps = float(self.dt), int(self.n_s), float(self.t_eps)
+        c.mode = 1 if self.mode == "adaptive" else 0
+        c.beta, c.dt_min, c.dt_max = float(self.beta), float(self.dt_min), float(self.dt_max)
+        c.ess, c.tile_size = int(bool(self.ess)), int(self.tile_size)
+        for k in range(3):
+            c.background[k] = float(self.background[k])
+        c.buffer_capacity = int(self.buffer_capacity)
+        return c
+
+
+@dataclass(frozen=True)
+class Ray:
+    """renderer.py:52-66."""
+
+    origin: np.ndarray
+    direction: np.ndarray
+    t_near: float
+    t_far: float
+
+    def __post_init__(self):
+        o = np.asarray(self.origin, dtype=float).reshape(3)
+        d = np.asarray(self.direction, dtype=float).reshape(3)
+        n = np.linalg.norm(d)
+        if abs(n - 1.0) > 1e-9:
+            d = d / n
+        object.__setattr__(self, "origin", o)
+        object.__setattr__(self, "direction", d)
+
+    def as_array(self) -> np.ndarray:
+        return np.concatenate([self.origin, self.direction, [self.t_near, self.t_far]])
+
+
+def quat_to_rotation(q) -> np.ndarray:
+    """geometry.py:26-42."""
+    q = np.asarray(q, dtype=float)
+    n = np.linalg.norm(q)
+    if n < 1e-12:
+        raise ValueError("zero quaternion")
+    w, x, y, z = q / n
+    return np.array([
+        [1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+        [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+        [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)],
+    ])
+
+
+@dataclass(frozen=True)
+class Camera:
+    """Pinhole camera (renderer.py:109-145): scalar-first camera-to-world quat,
+    looks along local +z, +y down; rays through pixel centres."""
+
+    center: np.ndarray
+    quat: np.ndarray
+    focal: float
+    width: int
+    height: int
+    t_near: float = 1e-4
+    t_far: float = 1e6
+
+    def __post_init__(self):
+        if self.focal <= 0:
+            raise ValueError("focal must be positive")
+        if self.width < 1 or self.height < 1:
+            raise ValueError("image dimensions must be >= 1")
+        object.__setattr__(self, "center", np.asarray(self.center, dtype=float).reshape(3))
+        q = np.asarray(self.quat, dtype=float).reshape(4)
+        object.__setattr__(self, "quat", q / np.linalg.norm(q))
+        object.__setattr__(self, "rotation", quat_to_rotation(self.quat))
+
+    def ray(self, px: int, py: int) -> Ray:
+        d_cam = np.array([(px + 0.5 - 0.5 * self.width) / self.focal,
+                          (py + 0.5 - 0.5 * self.height) / self.focal, 1.0])
+        d = self.rotation @ d_cam
+        d = d / np.linalg.norm(d)
+        return Ray(self.center, d, self.t_near, self.t_far)
+
+    def to_c(self) -> CameraC:
+        c = CameraC()
+        R = np.ascontiguousarray(self.rotation, dtype=np.float64).ravel()
+        for k in range(9):
+            c.R[k] = float(R[k])
+        for k in range(3):
+            c.center[k] = float(self.center[k])
+        c.focal = float(self.focal)
+        c.width, c.height = int(self.width), int(self.height)
+        c.t_near, c.t_far = float(self.t_near), float(self.t_far)
+        return c
+
+    @property
+    def n_tiles(self) -> int:
+        return ((self.width + 15) // 16) * ((self.height + 15) // 16)
+
+
+_STAT_KEYS = ("rays", "samples", "segments", "segments_skipped", "closest_hit_calls",
+              "node_visits", "aabb_hits", "ellipsoid_hits")
+
+
+@dataclass
+class RenderStats:
+    """renderer.py:69-106.  `node_visits` counts visits of the LBVH, which has a
+    different topology from the reference's SAH tree."""
+
+    rays: int = 0
+    samples: int = 0
+    segments: int = 0
+    segments_skipped: int = 0
+    closest_hit_calls: int = 0
+    node_visits: int = 0
+    aabb_hits: int = 0
+    ellipsoid_hits: int = 0
+    transmittance: float = 1.0
+
+    @property
+    def false_positives(self) -> int:
+        return self.aabb_hits - self.ellipsoid_hits
+
+    def merge(self, other: "RenderStats"):
+        for k in _STAT_KEYS + ("pairs", "composited"):
+            setattr(self, k, getattr(self, k) + getattr(other, k))
+
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k in _STAT_KEYS}
+        d["false_positives"] = self.false_positives
+        return d
+
+    pairs: int = 0
+    composited: int = 0
+
+    @classmethod
+    def from_counts(cls, counts) -> "RenderStats":
+        """From the 10 device counters (gsx_stats)."""
+        keys = _STAT_KEYS + ("pairs", "composited")
+        return cls(**{k: int(v) for k, v in zip(keys, counts)})
+
+
+def segment_step(cfg: RenderConfig, d_i: float, t_i: float) -> float:
+    """renderer.py:148-157 (host mirror; the kernel evaluates the same formula)."""
+    t = max(t_i, cfg.t_eps)
+    boost = math.exp(-math.log(t) / 3.0)
+    step = min(max(d_i / cfg.beta, cfg.dt_min) * boost, cfg.dt_max)
+    return cfg.n_s * step

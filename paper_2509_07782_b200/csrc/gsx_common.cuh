@@ -1,0 +1,201 @@
+// gsx_common.cuh -- shared device layouts and helpers for libgsx (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gsx.h"
+
+#define GSX_NREC 87
+#define GSX_NCOEF 76
+#define GSX_NONE ((int32_t)0x80000000)
+#define GSX_STACK 96
+
+// ---------------------------------------------------------------------------
+// Scene arena (caller-allocated, gsx_scene_arena_bytes).  N primitives in
+// storage order.  Sections are 256-byte aligned.
+//   aabb64 : double[n][6]  lo xyz, hi xyz   (scene.py:61-65, exact fp64)
+//   inv64  : double[n][9]  iso_inv          (scene.py:58-60, exact fp64)
+//   lr64   : double[n]     log_ratio        (scene.py:55)
+//   geo    : float4[n][4]  (mu, sigma~) (M row0, k*log2e/2) (M row1, 0) (M row2, 0)
+//   box32  : float[n][6]   outward-rounded fp32 AABB (LBVH leaves)
+//   app    : float4[n][19] sh 27 | unit sg axes 21 | sharpness 7 | amp 21
+//   bounds : double[6]     scene AABB lo xyz, hi xyz (scene.py:66-67)
+//   part   : double[GSX_BOUNDS_BLOCKS][6] partial bounds
+// ---------------------------------------------------------------------------
+#define GSX_BOUNDS_BLOCKS 296
+
+struct SceneView {
+  double* aabb64;
+  double* inv64;
+  double* lr64;
+  float4* geo;
+  float* box32;
+  float4* app;
+  double* bounds;
+  double* part;
+};
+
+static inline size_t gsx_align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline size_t gsx_al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline SceneView scene_view(void* arena, int64_t n) {
+  char* p = (char*)arena;
+  SceneView v;
+  size_t off = 0;
+  v.aabb64 = (double*)(p + off); off += gsx_al(sizeof(double) * 6 * n);
+  v.inv64 = (double*)(p + off);  off += gsx_al(sizeof(double) * 9 * n);
+  v.lr64 = (double*)(p + off);   off += gsx_al(sizeof(double) * n);
+  v.geo = (float4*)(p + off);    off += gsx_al(sizeof(float4) * 4 * n);
+  v.box32 = (float*)(p + off);   off += gsx_al(sizeof(float) * 6 * n);
+  v.app = (float4*)(p + off);    off += gsx_al(sizeof(float4) * 19 * n);
+  v.bounds = (double*)(p + off); off += gsx_al(sizeof(double) * 6);
+  v.part = (double*)(p + off);
+  return v;
+}
+
+inline size_t scene_arena_bytes_impl(int64_t n) {
+  size_t s = 0;
+  s += gsx_align256(sizeof(double) * 6 * n);
+  s += gsx_align256(sizeof(double) * 9 * n);
+  s += gsx_align256(sizeof(double) * n);
+  s += gsx_align256(sizeof(float4) * 4 * n);
+  s += gsx_align256(sizeof(float) * 6 * n);
+  s += gsx_align256(sizeof(float4) * 19 * n);
+  s += gsx_align256(sizeof(double) * 6);
+  s += gsx_align256(sizeof(double) * 6 * GSX_BOUNDS_BLOCKS);
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// BVH arena: internal nodes float4[n-1][4]:
+//   q0 = (lo_l.xyz, child_l)  q1 = (hi_l.xyz, child_r)
+//   q2 = (lo_r.xyz, 0)        q3 = (hi_r.xyz, 0)
+// child >= 0: internal node index; child < 0: leaf ~prim; GSX_NONE: absent.
+// parents int32[2n-1] (internal 0..n-2, leaf i at n-1+i).  Root = node 0.
+// For n == 1 a single node holds leaf 0 on the left and GSX_NONE on the right.
+// ---------------------------------------------------------------------------
+struct BvhView {
+  float4* nodes;
+  int32_t* parents;
+};
+
+__host__ __device__ inline int64_t bvh_internal_count(int64_t n) { return n > 1 ? n - 1 : 1; }
+
+__host__ __device__ inline BvhView bvh_view(void* arena, int64_t n) {
+  char* p = (char*)arena;
+  BvhView v;
+  size_t a = ((sizeof(float4) * 4 * bvh_internal_count(n)) + 255) & ~(size_t)255;
+  v.nodes = (float4*)p;
+  v.parents = (int32_t*)(p + a);
+  return v;
+}
+
+inline size_t bvh_arena_bytes_impl(int64_t n) {
+  return gsx_align256(sizeof(float4) * 4 * bvh_internal_count(n)) +
+         gsx_align256(sizeof(int32_t) * (2 * n + 1));
+}
+
+// ---------------------------------------------------------------------------
+// device status helpers
+// ---------------------------------------------------------------------------
+__device__ inline void dev_fail(gsx_dev_status* st, int64_t code, int64_t index, int64_t count = 0,
+                                int64_t cap = 0) {
+  if (!st) return;
+  // keep the smallest index of the first error code seen
+  unsigned long long* c = (unsigned long long*)&st->code;
+  unsigned long long old = atomicCAS(c, 0ull, (unsigned long long)code);
+  if (old == 0ull || old == (unsigned long long)code) {
+    atomicMin((long long*)&st->index, (long long)index);
+    if (count) {
+      atomicMax((long long*)&st->count, (long long)count);
+      st->capacity = cap;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 slab test mirroring spatial.py:258-277 (_box_slab), no contraction.
+// ---------------------------------------------------------------------------
+__device__ inline void box_slab64(const double* lo, const double* hi, const double* o,
+                                  const double* d, const double* inv, double& ta, double& tb) {
+  double t0 = -INFINITY, t1 = INFINITY;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (d[k] != 0.0) {
+      double a = __dmul_rn(__dsub_rn(lo[k], o[k]), inv[k]);
+      double b = __dmul_rn(__dsub_rn(hi[k], o[k]), inv[k]);
+      if (a > b) {
+        double t = a;
+        a = b;
+        b = t;
+      }
+      if (a > t0) t0 = a;
+      if (b < t1) t1 = b;
+    } else if (o[k] < lo[k] || o[k] > hi[k]) {
+      ta = INFINITY;
+      tb = -INFINITY;
+      return;
+    }
+  }
+  ta = t0;
+  tb = t1;
+}
+
+// inverse direction for traversal queries (spatial.py:227, :321)
+__device__ inline void inv_dir_traversal64(const double* d, double* inv) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) inv[k] = fabs(d[k]) > 1e-300 ? 1.0 / (d[k] == 0.0 ? 1.0 : d[k]) : INFINITY;
+}
+
+// spatial.py:280-306 ray_ellipsoid_interval, fp64, no contraction.
+__device__ inline bool ray_ellipsoid_interval64(const double* ol, const double* dl, double t_lo,
+                                                double t_hi, double& tin, double& tout) {
+  double a = __dadd_rn(__dadd_rn(__dmul_rn(dl[0], dl[0]), __dmul_rn(dl[1], dl[1])),
+                       __dmul_rn(dl[2], dl[2]));
+  double b = __dadd_rn(__dadd_rn(__dmul_rn(ol[0], dl[0]), __dmul_rn(ol[1], dl[1])),
+                       __dmul_rn(ol[2], dl[2]));
+  double c = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(ol[0], ol[0]), __dmul_rn(ol[1], ol[1])),
+                                 __dmul_rn(ol[2], ol[2])),
+                       1.0);
+  double disc = __dsub_rn(__dmul_rn(b, b), __dmul_rn(a, c));
+  if (disc < 0.0 || a == 0.0) return false;
+  double sq = sqrt(disc);
+  double q = (b >= 0.0) ? -__dadd_rn(b, sq) : -__dsub_rn(b, sq);
+  double t0 = __ddiv_rn(q, a);
+  double t1 = (q != 0.0) ? __ddiv_rn(c, q) : t0;
+  if (t0 > t1) {
+    double t = t0;
+    t0 = t1;
+    t1 = t;
+  }
+  if (t_lo > t0) t0 = t_lo;
+  if (t_hi < t1) t1 = t_hi;
+  if (t0 > t1) return false;
+  tin = t0;
+  tout = t1;
+  return true;
+}
+
+// fp64 slab of an fp32 node box (exact conversion; conservative for the
+// outward-rounded boxes).
+__device__ inline void box_slab64_f(const float4 lo, const float4 hi, const double* o,
+                                    const double* d, const double* inv, double& ta, double& tb) {
+  double l[3] = {(double)lo.x, (double)lo.y, (double)lo.z};
+  double h[3] = {(double)hi.x, (double)hi.y, (double)hi.z};
+  box_slab64(l, h, o, d, inv, ta, tb);
+}
+
+__device__ inline int32_t f_as_i(float f) { return __float_as_int(f); }
+
+#define CUDA_CHECK_RET(expr)                       \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) {                       \
+      gsx_set_cuda_error(_e);                      \
+      return GSX_ERR_CUDA;                         \
+    }                                              \
+  } while (0)
+
+void gsx_set_cuda_error(cudaError_t e);
+int gsx_check_launch();

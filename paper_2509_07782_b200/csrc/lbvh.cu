@@ -1,0 +1,162 @@
+// lbvh.cu -- K5: linear BVH over Morton-ordered primitives (replaces the
+// recursive binned-SAH Bvh of spatial.py:126-211, which takes 13 s at 100k).
+//
+// Topology: Karras (2012) -- internal node i's key range and split are found
+// from the longest-common-prefix function delta over the sorted 63-bit codes
+// (ties broken by index), one thread per internal node.  Boxes: bottom-up
+// refit, one thread per leaf, the second thread to reach a node (atomic
+// counter) merges its two children.  Leaves are single primitives in storage
+// order; each internal node stores both child boxes (fp32, outward-rounded
+// from the fp64 AABBs) so one 64-byte load tests both children.
+#include "gsx_common.cuh"
+
+namespace {
+
+__device__ inline int delta(const uint64_t* __restrict__ codes, int64_t n, int64_t i, int64_t j) {
+  if (j < 0 || j >= n) return -1;
+  uint64_t a = codes[i], b = codes[j];
+  if (a == b) return 64 + __clz((unsigned)(i ^ j));
+  return __clzll((long long)(a ^ b));
+}
+
+__global__ void k_karras(const uint64_t* __restrict__ codes, const int64_t* __restrict__ perm,
+                         int64_t n, float4* nodes, int32_t* parents) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = (delta(codes, n, i, i + 1) - delta(codes, n, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = delta(codes, n, i, i - d);
+  int64_t lmax = 2;
+  while (delta(codes, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int64_t l = 0;
+  for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
+    if (delta(codes, n, i, i + (l + t) * d) > dmin) l += t;
+  int64_t j = i + l * d;
+  int dnode = delta(codes, n, i, j);
+  int64_t s = 0;
+  int64_t t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (delta(codes, n, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  int64_t gamma = i + s * d + (d < 0 ? -1 : 0);
+  int64_t lo = i < j ? i : j, hi = i < j ? j : i;
+  // leaves reference storage indices (perm maps sorted position -> storage)
+  bool lleaf = lo == gamma, rleaf = hi == gamma + 1;
+  int32_t left = lleaf ? ~(int32_t)(perm ? perm[gamma] : gamma) : (int32_t)gamma;
+  int32_t right = rleaf ? ~(int32_t)(perm ? perm[gamma + 1] : gamma + 1) : (int32_t)(gamma + 1);
+  float4* nd = nodes + 4 * i;
+  nd[0].w = __int_as_float(left);
+  nd[1].w = __int_as_float(right);
+  parents[lleaf ? (n - 1) + gamma : gamma] = (int32_t)i;
+  parents[rleaf ? (n - 1) + gamma + 1 : gamma + 1] = (int32_t)i;
+  if (i == 0) parents[0] = -1;
+}
+
+struct Box {
+  float lo[3], hi[3];
+};
+
+__device__ inline Box leaf_box(const float* box32, int64_t prim) {
+  Box b;
+  for (int k = 0; k < 3; ++k) {
+    b.lo[k] = box32[6 * prim + k];
+    b.hi[k] = box32[6 * prim + 3 + k];
+  }
+  return b;
+}
+
+__device__ inline Box node_union(const float4* nodes, int32_t c) {
+  // read with L1 bypass: written by another thread of this kernel
+  const float4* nd = nodes + 4 * (int64_t)c;
+  float4 a = __ldcg(nd + 0), b = __ldcg(nd + 1), e = __ldcg(nd + 2), f = __ldcg(nd + 3);
+  Box r;
+  r.lo[0] = fminf(a.x, e.x);
+  r.lo[1] = fminf(a.y, e.y);
+  r.lo[2] = fminf(a.z, e.z);
+  r.hi[0] = fmaxf(b.x, f.x);
+  r.hi[1] = fmaxf(b.y, f.y);
+  r.hi[2] = fmaxf(b.z, f.z);
+  return r;
+}
+
+__global__ void k_refit(const float* __restrict__ box32, int64_t n, float4* nodes,
+                        const int32_t* __restrict__ parents, int32_t* flags) {
+  int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= n) return;
+  int32_t p = parents[(n - 1) + leaf];
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(&flags[p], 1) == 0) return;  // first arrival: sibling not ready
+    __threadfence();
+    float4* nd = nodes + 4 * (int64_t)p;
+    int32_t cl = __float_as_int(__ldcg(&nd[0].w)), cr = __float_as_int(__ldcg(&nd[1].w));
+    Box bl = cl < 0 ? leaf_box(box32, ~cl) : node_union(nodes, cl);
+    Box br = cr < 0 ? leaf_box(box32, ~cr) : node_union(nodes, cr);
+    __stcg(nd + 0, make_float4(bl.lo[0], bl.lo[1], bl.lo[2], __int_as_float(cl)));
+    __stcg(nd + 1, make_float4(bl.hi[0], bl.hi[1], bl.hi[2], __int_as_float(cr)));
+    __stcg(nd + 2, make_float4(br.lo[0], br.lo[1], br.lo[2], 0.f));
+    __stcg(nd + 3, make_float4(br.hi[0], br.hi[1], br.hi[2], 0.f));
+    p = parents[p];
+  }
+}
+
+__global__ void k_single(const float* __restrict__ box32, float4* nodes, int32_t* parents) {
+  Box b = leaf_box(box32, 0);
+  nodes[0] = make_float4(b.lo[0], b.lo[1], b.lo[2], __int_as_float(~0));
+  nodes[1] = make_float4(b.hi[0], b.hi[1], b.hi[2], __int_as_float(GSX_NONE));
+  nodes[2] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+  nodes[3] = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+  parents[0] = -1;
+  parents[1] = 0;  // leaf 0 (slot n-1+0 == 0 would collide; n==1 uses slot 1)
+}
+
+__global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* children) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const float4* nd = nodes + 4 * i;
+  float4 a = nd[0], b = nd[1], c = nd[2], d = nd[3];
+  float* o = boxes + 12 * i;
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = b.x; o[4] = b.y; o[5] = b.z;
+  o[6] = c.x; o[7] = c.y; o[8] = c.z; o[9] = d.x; o[10] = d.y; o[11] = d.z;
+  children[2 * i] = __float_as_int(a.w);
+  children[2 * i + 1] = __float_as_int(b.w);
+}
+
+}  // namespace
+
+extern "C" size_t gsx_bvh_arena_bytes(int64_t n) { return bvh_arena_bytes_impl(n); }
+extern "C" size_t gsx_bvh_workspace_bytes(int64_t n) {
+  return gsx_align256(sizeof(int32_t) * (n > 1 ? n : 1));
+}
+
+extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_codes,
+                             const int64_t* perm, int64_t n, void* bvh_arena, void* workspace,
+                             void* stream) {
+  if (n <= 0) return GSX_ERR_EMPTY;
+  if (n >= 0x7fffffffLL) return GSX_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  SceneView sv = scene_view((void*)scene_arena, n);
+  BvhView bv = bvh_view(bvh_arena, n);
+  if (n == 1) {
+    k_single<<<1, 1, 0, s>>>(sv.box32, bv.nodes, bv.parents);
+    return gsx_check_launch();
+  }
+  int32_t* flags = (int32_t*)workspace;
+  CUDA_CHECK_RET(cudaMemsetAsync(flags, 0, sizeof(int32_t) * (n - 1), s));
+  k_karras<<<(unsigned)((n - 1 + 255) / 256), 256, 0, s>>>(sorted_codes, perm, n, bv.nodes,
+                                                           bv.parents);
+  k_refit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sv.box32, n, bv.nodes, bv.parents, flags);
+  return gsx_check_launch();
+}
+
+extern "C" int gsx_bvh_export(const void* bvh_arena, int64_t n, float* boxes, int32_t* children,
+                              int32_t* parents, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  BvhView bv = bvh_view((void*)bvh_arena, n);
+  int64_t m = bvh_internal_count(n);
+  k_export<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(bv.nodes, m, boxes, children);
+  if (parents)
+    CUDA_CHECK_RET(cudaMemcpyAsync(parents, bv.parents, sizeof(int32_t) * (n > 1 ? 2 * n - 1 : 2),
+                                   cudaMemcpyDeviceToDevice, s));
+  return gsx_check_launch();
+}

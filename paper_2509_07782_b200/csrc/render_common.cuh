@@ -1,0 +1,407 @@
+// render_common.cuh -- per-ray device building blocks shared by the forward
+// (render.cu) and backward (render_bwd.cu) kernels.
+#pragma once
+#include "gsx_common.cuh"
+
+namespace gsx {
+
+// ---------------------------------------------------------------------------
+// ray context: fp64 ray (reference semantics) + fp32 copies for traversal
+// ---------------------------------------------------------------------------
+struct RayCtx {
+  double o[3], d[3];
+  double inv_t[3];  // traversal-style inverse (spatial.py:227)
+  float of[3], df[3], invf[3];
+  float eps_scale;
+  double t_n, t_f;
+};
+
+__device__ inline double norm3d(const double* v) {
+  return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(v[0], v[0]), __dmul_rn(v[1], v[1])),
+                        __dmul_rn(v[2], v[2])));
+}
+
+// Ray.__post_init__ renormalization (renderer.py:60-64) + clip_ray_to_scene
+// (renderer.py:160-175).  Returns false when the ray misses (background).
+__device__ inline bool finish_ray(const double* bounds, bool clip, double t_near, double t_far,
+                                  RayCtx& r) {
+  double n = norm3d(r.d);
+  if (fabs(n - 1.0) > 1e-9)
+    for (int k = 0; k < 3; ++k) r.d[k] = r.d[k] / n;
+  if (t_near >= t_far) return false;
+  if (clip) {
+    double inv[3];
+    for (int k = 0; k < 3; ++k) inv[k] = r.d[k] == 0.0 ? INFINITY : 1.0 / r.d[k];
+    double a, b;
+    box_slab64(bounds, bounds + 3, r.o, r.d, inv, a, b);
+    double t0 = t_near > a ? t_near : a;
+    double t1 = t_far < b ? t_far : b;
+    if (t0 >= t1) return false;
+    r.t_n = t0;
+    r.t_f = t1;
+  } else {
+    r.t_n = t_near;
+    r.t_f = t_far;
+  }
+  inv_dir_traversal64(r.d, r.inv_t);
+  float sc = 1.f;
+  for (int k = 0; k < 3; ++k) {
+    r.of[k] = (float)r.o[k];
+    r.df[k] = (float)r.d[k];
+    float dd = fabsf(r.df[k]) > 1e-30f ? r.df[k] : copysignf(1e-30f, r.df[k]);
+    r.invf[k] = 1.0f / dd;
+    sc = fmaxf(sc, fabsf(r.of[k]));
+  }
+  r.eps_scale = sc;
+  return true;
+}
+
+// Camera.ray (renderer.py:135-145) for pixel (px, py).
+__device__ inline bool camera_ray(const gsx_camera& cam, double px, double py,
+                                  const double* bounds, RayCtx& r) {
+  double dc[3] = {__ddiv_rn(__dsub_rn(__dadd_rn(px, 0.5), 0.5 * (double)cam.width), cam.focal),
+                  __ddiv_rn(__dsub_rn(__dadd_rn(py, 0.5), 0.5 * (double)cam.height), cam.focal),
+                  1.0};
+  double d[3];
+  for (int a = 0; a < 3; ++a)
+    d[a] = __dadd_rn(__dadd_rn(__dmul_rn(cam.R[3 * a], dc[0]), __dmul_rn(cam.R[3 * a + 1], dc[1])),
+                     __dmul_rn(cam.R[3 * a + 2], dc[2]));
+  double n = norm3d(d);
+  for (int k = 0; k < 3; ++k) {
+    r.o[k] = cam.center[k];
+    r.d[k] = d[k] / n;
+  }
+  return finish_ray(bounds, true, cam.t_near, cam.t_far, r);
+}
+
+__device__ inline bool explicit_ray(const double* ray8, bool clip, const double* bounds,
+                                    RayCtx& r) {
+  for (int k = 0; k < 3; ++k) {
+    r.o[k] = ray8[k];
+    r.d[k] = ray8[3 + k];
+  }
+  return finish_ray(bounds, clip, ray8[6], ray8[7], r);
+}
+
+// Z-order position of thread t in a 16x16 tile (x: even bits, y: odd bits)
+__device__ inline void morton_decode8(unsigned t, int& x, int& y) {
+  x = (t & 1) | ((t >> 1) & 2) | ((t >> 2) & 4) | ((t >> 3) & 8);
+  y = ((t >> 1) & 1) | ((t >> 2) & 2) | ((t >> 3) & 4) | ((t >> 4) & 8);
+}
+
+__device__ inline float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// appearance (appearance.py:26-50, 91-98), fp32
+// ---------------------------------------------------------------------------
+__device__ inline void sh_basis_f(const float* d, float* Y) {
+  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f, C2A = 1.0925484305920792f,
+              C2B = 0.31539156525252005f, C2C = 0.5462742152960396f;
+  float x = d[0], y = d[1], z = d[2];
+  Y[0] = C0;
+  Y[1] = C1 * y;
+  Y[2] = C1 * z;
+  Y[3] = C1 * x;
+  Y[4] = C2A * x * y;
+  Y[5] = C2A * y * z;
+  Y[6] = C2B * (3.0f * z * z - 1.0f);
+  Y[7] = C2A * x * z;
+  Y[8] = C2C * (x * x - y * y);
+}
+
+// unclamped radiance and lobe values (for the backward); app = 19 float4
+__device__ inline void eval_radiance_pre(const float4* __restrict__ app, const float* Y,
+                                         const float* d, float* pre, float* lobes) {
+  float a[76];
+#pragma unroll
+  for (int k = 0; k < 19; ++k) {
+    float4 v = __ldg(app + k);
+    a[4 * k] = v.x;
+    a[4 * k + 1] = v.y;
+    a[4 * k + 2] = v.z;
+    a[4 * k + 3] = v.w;
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float s = 0.f;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) s = fmaf(Y[b], a[3 * b + ch], s);
+    pre[ch] = s;
+  }
+#pragma unroll
+  for (int l = 0; l < 7; ++l) {
+    float cs = a[27 + 3 * l] * d[0] + a[28 + 3 * l] * d[1] + a[29 + 3 * l] * d[2];
+    float e = __expf(a[48 + l] * (cs - 1.0f));
+    if (lobes) lobes[l] = e;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) pre[ch] = fmaf(e, a[55 + 3 * l + ch], pre[ch]);
+  }
+}
+
+__device__ inline void eval_radiance_f(const float4* __restrict__ app, const float* Y,
+                                       const float* d, float* c) {
+  float pre[3];
+  eval_radiance_pre(app, Y, d, pre, nullptr);
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) c[ch] = fmaxf(pre[ch], 0.f);
+}
+
+// ---------------------------------------------------------------------------
+// per-(ray, primitive) density setup: q(t) = A (t - tc)^2 + qmin
+// ---------------------------------------------------------------------------
+struct CandSetup {
+  float A, qmin, del0, kl2, sigma, h;
+  double tc;
+};
+
+__device__ inline void local_frame(const float4* geo, int64_t p, const RayCtx& r, double* y0,
+                                   double* yd) {
+  float4 g0 = __ldg(geo + 4 * p), g1 = __ldg(geo + 4 * p + 1), g2 = __ldg(geo + 4 * p + 2),
+         g3 = __ldg(geo + 4 * p + 3);
+  double v[3] = {r.o[0] - (double)g0.x, r.o[1] - (double)g0.y, r.o[2] - (double)g0.z};
+  double M[9] = {g1.x, g1.y, g1.z, g2.x, g2.y, g2.z, g3.x, g3.y, g3.z};
+  for (int a = 0; a < 3; ++a) {
+    y0[a] = fma(M[3 * a], v[0], fma(M[3 * a + 1], v[1], M[3 * a + 2] * v[2]));
+    yd[a] = fma(M[3 * a], r.d[0], fma(M[3 * a + 1], r.d[1], M[3 * a + 2] * r.d[2]));
+  }
+}
+
+__device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t p, double tbase,
+                                  CandSetup& cs) {
+  double y0[3], yd[3];
+  local_frame(sv.geo, p, r, y0, yd);
+  double A = yd[0] * yd[0] + yd[1] * yd[1] + yd[2] * yd[2];
+  if (!(A > 0.0)) return false;
+  double B = y0[0] * yd[0] + y0[1] * yd[1] + y0[2] * yd[2];
+  double C = y0[0] * y0[0] + y0[1] * y0[1] + y0[2] * y0[2];
+  double tc = -B / A;
+  double qmin = fma(B, tc, C);
+  if (qmin > 1.0) return false;
+  float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1);
+  cs.A = (float)A;
+  cs.qmin = (float)qmin;
+  cs.tc = tc;
+  cs.del0 = (float)(tbase - tc);
+  cs.kl2 = g1.w;
+  cs.sigma = g0.w;
+  cs.h = sqrtf(fmaxf((float)((1.0 - qmin) / A), 0.f));
+  return true;
+}
+
+// conservative sample index range [jlo, jhi] within [0, m-1] that may lie
+// inside the ellipsoid (the q <= 1 test decides exactly).
+__device__ inline bool sample_range(const CandSetup& cs, float dtf, int m, int& jlo, int& jhi) {
+  float lo = (-cs.h - cs.del0) / dtf;
+  float hi = (cs.h - cs.del0) / dtf;
+  if (!(hi >= -1.f) || !(lo <= (float)m)) return false;
+  lo = fmaxf(lo, -1.f);
+  hi = fminf(hi, (float)m);
+  jlo = max(0, (int)floorf(lo));
+  jhi = min(m - 1, (int)ceilf(hi));
+  return jlo <= jhi;
+}
+
+// ---------------------------------------------------------------------------
+// exact fp64 tests (reference arithmetic) used for ESS emptiness and stats
+// ---------------------------------------------------------------------------
+__device__ inline bool exact_aabb_overlap(const SceneView& sv, const RayCtx& r, int64_t p,
+                                          double t0, double t1) {
+  const double* ab = sv.aabb64 + 6 * p;
+  double ta, tb;
+  box_slab64(ab, ab + 3, r.o, r.d, r.inv_t, ta, tb);
+  return ta <= t1 && tb >= t0;
+}
+
+__device__ inline bool ellipsoid_hits_interval(const SceneView& sv, const RayCtx& r, int64_t p,
+                                               double t0, double t1) {
+  const double* M = sv.inv64 + 9 * p;
+  float4 g = sv.geo[4 * p];
+  double v[3] = {__dsub_rn(r.o[0], (double)g.x), __dsub_rn(r.o[1], (double)g.y),
+                 __dsub_rn(r.o[2], (double)g.z)};
+  double ol[3], dl[3];
+  for (int a = 0; a < 3; ++a) {
+    ol[a] = __dadd_rn(__dadd_rn(__dmul_rn(M[3 * a], v[0]), __dmul_rn(M[3 * a + 1], v[1])),
+                      __dmul_rn(M[3 * a + 2], v[2]));
+    dl[a] = __dadd_rn(__dadd_rn(__dmul_rn(M[3 * a], r.d[0]), __dmul_rn(M[3 * a + 1], r.d[1])),
+                      __dmul_rn(M[3 * a + 2], r.d[2]));
+  }
+  double a, b;
+  return ray_ellipsoid_interval64(ol, dl, t0, t1, a, b);
+}
+
+// segment_step (renderer.py:148-157)
+__device__ inline double segment_step(const gsx_render_cfg& cfg, double d_i, double t_i) {
+  double t = t_i > cfg.t_eps ? t_i : cfg.t_eps;
+  double boost = exp(-log(t) / 3.0);
+  double a = d_i / cfg.beta;
+  if (!(a > cfg.dt_min)) a = cfg.dt_min;
+  double step = a * boost;
+  if (step > cfg.dt_max) step = cfg.dt_max;
+  return (double)cfg.n_s * step;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 traversal
+// ---------------------------------------------------------------------------
+__device__ inline void slab_f(const float4& lo, const float4& hi, const RayCtx& r, float& tmin,
+                              float& tmax) {
+  float x0 = (lo.x - r.of[0]) * r.invf[0], x1 = (hi.x - r.of[0]) * r.invf[0];
+  float y0 = (lo.y - r.of[1]) * r.invf[1], y1 = (hi.y - r.of[1]) * r.invf[1];
+  float z0 = (lo.z - r.of[2]) * r.invf[2], z1 = (hi.z - r.of[2]) * r.invf[2];
+  tmin = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+  tmax = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+}
+
+__device__ inline float margin(const RayCtx& r, float t) {
+  return 2e-6f * (fabsf(t) + r.eps_scale);
+}
+
+// Visit every leaf whose (outward-rounded) box slab interval overlaps
+// [t0, t1] (with a conservative margin); leaf_fn(prim) is called in traversal
+// order.  Returns false if the stack overflowed.
+template <class F>
+__device__ inline bool traverse_segment(const BvhView& bv, const RayCtx& r, float t0, float t1,
+                                        F&& leaf_fn, uint32_t& visits) {
+  const float lo_t = t0 - margin(r, t0), hi_t = t1 + margin(r, t1);
+  int32_t stack[GSX_STACK];
+  int sp = 0;
+  int32_t node = 0;
+  bool ok = true;
+  for (;;) {
+    ++visits;
+    const float4* nd = bv.nodes + 4 * (int64_t)node;
+    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), e = __ldg(nd + 3);
+    int32_t cl = __float_as_int(a.w), cr = __float_as_int(b.w);
+    float mn, mx;
+    slab_f(a, b, r, mn, mx);
+    bool hl = cl != GSX_NONE && mn <= hi_t && mx >= lo_t;
+    slab_f(c, e, r, mn, mx);
+    bool hr = cr != GSX_NONE && mn <= hi_t && mx >= lo_t;
+    int32_t next = -1;
+    if (hl) {
+      if (cl < 0)
+        leaf_fn((int64_t)(~cl));
+      else
+        next = cl;
+    }
+    if (hr) {
+      if (cr < 0)
+        leaf_fn((int64_t)(~cr));
+      else if (next >= 0) {
+        if (sp < GSX_STACK)
+          stack[sp++] = cr;
+        else
+          ok = false;
+      } else
+        next = cr;
+    }
+    if (next < 0) {
+      if (sp == 0) break;
+      next = stack[--sp];
+    }
+    node = next;
+  }
+  return ok;
+}
+
+// closest ellipsoid entry in [t_lo, t_hi] (spatial.py:309-354): fp32 node
+// tests with margin, near child first, pruning by the current best; leaves
+// use the fp64 Kahan interval in the primitive's unit-sphere frame.
+__device__ inline bool closest_hit_r(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+                                     double t_lo, double t_hi, double& hit, uint32_t& visits) {
+  if (t_lo > t_hi) return false;
+  double best = INFINITY;
+  int32_t snode[GSX_STACK];
+  float sent[GSX_STACK];
+  int sp = 0;
+  int32_t node = 0;
+  const float lo_t = (float)t_lo - margin(r, (float)t_lo);
+  for (;;) {
+    ++visits;
+    const float4* nd = bv.nodes + 4 * (int64_t)node;
+    float4 a = __ldg(nd), b = __ldg(nd + 1), c = __ldg(nd + 2), e = __ldg(nd + 3);
+    int32_t ch[2] = {__float_as_int(a.w), __float_as_int(b.w)};
+    float mn[2], mx[2];
+    slab_f(a, b, r, mn[0], mx[0]);
+    slab_f(c, e, r, mn[1], mx[1]);
+    bool go[2] = {false, false};
+    for (int k = 0; k < 2; ++k) {
+      int32_t cc = ch[k];
+      if (cc == GSX_NONE) continue;
+      double lim = t_hi < best ? t_hi : best;
+      float limf = (float)lim + margin(r, (float)lim);
+      if (!(mn[k] <= limf && mx[k] >= lo_t)) continue;
+      if (cc < 0) {
+        int64_t p = ~(int64_t)cc;
+        double y0[3], yd[3];
+        local_frame(sv.geo, p, r, y0, yd);
+        double tin, tout;
+        if (ray_ellipsoid_interval64(y0, yd, t_lo, lim, tin, tout) && tin < best) best = tin;
+      } else {
+        go[k] = true;
+      }
+    }
+    int32_t next = -1;
+    if (go[0] && go[1]) {
+      int nr = mn[1] < mn[0] ? 1 : 0;
+      if (sp < GSX_STACK) {
+        snode[sp] = ch[1 - nr];
+        sent[sp++] = mn[1 - nr];
+      }
+      next = ch[nr];
+    } else if (go[0]) {
+      next = ch[0];
+    } else if (go[1]) {
+      next = ch[1];
+    }
+    while (next < 0 && sp > 0) {
+      --sp;
+      float ent = sent[sp];
+      double lim = t_hi < best ? t_hi : best;
+      if (ent <= (float)lim + margin(r, (float)lim)) next = snode[sp];
+    }
+    if (next < 0) break;
+    node = next;
+  }
+  if (best < INFINITY) {
+    hit = best;
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// front-to-back accumulator (renderer.py:230-239) + depth
+// ---------------------------------------------------------------------------
+struct RayAccum {
+  float C[3];
+  float D;
+  float od;
+  float T;
+  __device__ void init() {
+    C[0] = C[1] = C[2] = 0.f;
+    D = 0.f;
+    od = 0.f;
+    T = 1.f;
+  }
+  __device__ float transmittance() const { return T; }
+  __device__ void add_sample(float sig, const float* W, float tj, float dt) {
+    if (sig > 0.f) {
+      float ods = sig * dt;
+      float w = -expm1f(-ods) * T;
+      float s = w / sig;
+      C[0] = fmaf(s, W[0], C[0]);
+      C[1] = fmaf(s, W[1], C[1]);
+      C[2] = fmaf(s, W[2], C[2]);
+      D = fmaf(w, tj, D);
+      od += ods;
+      T = expf(-od);
+    }
+  }
+};
+
+}  // namespace gsx

@@ -119,7 +119,8 @@ def _random_appearance_block(rng: np.random.Generator, n: int) -> np.ndarray:
 def synth_records(kind: str, count: int, seed: int = 0, anisotropy: float = 1.0,
                   extent: float = 1.0, base_scale: float | None = None,
                   sigma_scale: float | None = None, r_max_bound: float | None = None,
-                  shell_fraction: float = 0.0, shell_radius=(10.0, 50.0)) -> np.ndarray:
+                  shell_fraction: float = 0.0, shell_radius=(10.0, 50.0),
+                  view_radius: float = 3.5) -> np.ndarray:
     """Vectorised large-N generator (float32-representable float64 records).
 
     Defaults follow SURVEY.md 8(d): base = 0.08 * (32/N)^(1/3) and
@@ -171,7 +172,8 @@ def synth_records(kind: str, count: int, seed: int = 0, anisotropy: float = 1.0,
         v /= np.linalg.norm(v, axis=1, keepdims=True)
         rad = rng.uniform(shell_radius[0], shell_radius[1], size=n_shell)
         means[n_in:] = v * rad[:, None]
-        scale_mul[n_in:] = rad / extent * 2.0
+        # same angular size as a foreground primitive seen from `view_radius`
+        scale_mul[n_in:] = rad / view_radius
     rec[:, 0:3] = means
     rec[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
     bb = b * scale_mul

@@ -1,0 +1,398 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle
+and the reference's golden vectors.
+
+Tolerances (BASELINE.json north star): Morton codes, sort permutations and
+per-segment candidate sets are bit-exact; closest hits within 1e-9;
+rendered RGB and transmittance within max-abs 1e-4 (fp32 kernels vs the fp64
+reference); depth (sum_j w_j t_j) within 1e-4 * t_far of the ray.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden
+from paper_2509_07782_b200.scenes import f32_records, gen_test_scene_records
+
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 1e-4
+T_TOL = 1e-4
+
+SPECS = {
+    "small": dict(kind="random-cloud", count=20, seed=1),
+    "grid": dict(kind="grid", count=27, seed=3),
+    "shell": dict(kind="shell", count=12, seed=5),
+    "single": dict(kind="single-gaussian"),
+    "q150": dict(kind="random-cloud", count=150, seed=11, anisotropy=3.0),
+    "q100": dict(kind="random-cloud", count=100, seed=7, anisotropy=3.0),
+    "q30": dict(kind="random-cloud", count=30, seed=17, anisotropy=3.0),
+    "c1": dict(kind="random-cloud", count=10_000, seed=0, anisotropy=3.0, base_scale=0.01177),
+}
+CFG = {
+    "uniform": {}, "uniform_noess": dict(ess=False), "adaptive": dict(mode="adaptive"),
+    "adaptive_noess": dict(mode="adaptive", ess=False),
+    "uniform_bg_cap2": dict(background=(0.1, 0.2, 0.3), buffer_capacity=2),
+}
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2509_07782_b200 as G
+
+    return G
+
+
+_scenes = {}
+
+
+def gscene(G, name):
+    if name not in _scenes:
+        _scenes[name] = G.Scene.from_records(f32_records(gen_test_scene_records(**SPECS[name])))
+    return _scenes[name]
+
+
+def camera_from(G, g, prefix):
+    return G.Camera(center=g[f"{prefix}.cam_center"], quat=g[f"{prefix}.cam_quat"],
+                    focal=float(g[f"{prefix}.cam_focal"]), width=int(g[f"{prefix}.cam_w"]),
+                    height=int(g[f"{prefix}.cam_h"]))
+
+
+# ---------------------------------------------------------------- K1 prep
+@pytest.mark.parametrize("name", ["small", "grid", "shell", "single", "q150"])
+def test_derived_arrays(G, name):
+    g = golden("derived")
+    s = gscene(G, name)
+    np.testing.assert_allclose(s.aabb_lo, g[f"{name}.aabb_lo"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(s.aabb_hi, g[f"{name}.aabb_hi"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(s.iso_inv, g[f"{name}.iso_inv"], rtol=1e-14, atol=1e-13)
+    np.testing.assert_allclose(s.log_ratio, g[f"{name}.log_ratio"], rtol=1e-15, atol=0)
+    np.testing.assert_allclose(s.bounds_lo, g[f"{name}.bounds_lo"], rtol=0, atol=1e-15)
+
+
+def test_c1_bounds_bit_exact(G):
+    g = golden("derived")
+    s = gscene(G, "c1")
+    assert np.array_equal(s.bounds_lo, g["c1.bounds_lo"])
+    assert np.array_equal(s.bounds_hi, g["c1.bounds_hi"])
+
+
+def test_validation_errors(G):
+    rec = f32_records(gen_test_scene_records(**SPECS["small"]))
+    bad = rec.copy()
+    bad[7, 10] = 0.005  # sigma~ <= sigma_eps (scene.py:37-41)
+    with pytest.raises(G.ValidationError) as e:
+        G.Scene.from_records(bad)
+    assert e.value.record == 7
+    bad = rec.copy()
+    bad[3, 3:7] = 0.0  # zero quaternion
+    with pytest.raises(G.ValidationError) as e:
+        G.Scene.from_records(bad)
+    assert e.value.record == 3
+    with pytest.raises(G.EmptyScene):
+        G.Scene.from_records(np.zeros((0, 87)))
+
+
+# ---------------------------------------------------------------- K2/K3 Morton + sort
+def test_morton_known_answers(G):
+    from paper_2509_07782_b200 import spatial
+
+    assert spatial.morton_encode([0, 0, 0]) == 0
+    assert spatial.morton_encode([1, 1, 1]) == 7
+    assert spatial.morton_encode([3, 1, 0]) == 11
+    assert list(spatial.morton_decode(11)) == [3, 1, 0]
+    mx = spatial.MORTON_MAX
+    for v in (0, 1, mx - 1, mx):
+        p = [v, mx - v, v // 2]
+        assert list(spatial.morton_decode(spatial.morton_encode(p))) == p
+    with pytest.raises(ValueError):
+        spatial.morton_encode([mx + 1, 0, 0])
+    g = golden("morton")
+    assert np.array_equal(spatial.morton_encode(g["enc_pts"]), g["enc_codes"])
+
+
+def test_c1_codes_and_perm_bit_exact(G):
+    from paper_2509_07782_b200 import spatial
+
+    g = golden("morton")
+    d = golden("derived")
+    s = gscene(G, "c1")
+    # from the reference's own bounds
+    codes = spatial.morton_codes(s.means, d["c1.bounds_lo"], d["c1.bounds_hi"])
+    assert np.array_equal(codes, g["c1.codes"])
+    assert np.array_equal(spatial.morton_order(s.means, d["c1.bounds_lo"], d["c1.bounds_hi"]),
+                          g["c1.perm"])
+    # and through the device build pipeline (device bounds)
+    assert np.array_equal(s.morton_codes(), g["c1.codes"])
+    assert np.array_equal(s.morton_perm.cpu().numpy(), g["c1.perm"])
+
+
+@pytest.mark.parametrize("name", ["small", "grid", "shell", "q150"])
+def test_reorder_by_morton(G, name):
+    g = golden("morton")
+    s = G.Scene.from_records(f32_records(gen_test_scene_records(**SPECS[name])))
+    assert np.array_equal(G.reorder_by_morton(s), g[f"{name}.perm"])
+    assert np.array_equal(G.reorder_by_morton(s), g[f"{name}.perm2"])
+    assert np.array_equal(s.uids, g[f"{name}.uids_after"])
+
+
+def test_sort_stability(G):
+    from paper_2509_07782_b200 import spatial
+
+    g = golden("morton")
+    pts = g["dup.pts"]
+    assert np.array_equal(spatial.morton_order(pts, pts.min(0), pts.max(0)), g["dup.perm"])
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 2047, 2048, 2049, 100_003, 1_000_000):
+        keys = rng.integers(0, 1 << 63, size=n, dtype=np.uint64)
+        keys[rng.uniform(size=n) < 0.3] = keys[0]  # heavy duplicates
+        sk, perm = spatial.sort_codes(keys)
+        want = np.argsort(keys, kind="stable")
+        assert np.array_equal(perm, want), n
+        assert np.array_equal(sk, keys[want]), n
+
+
+# ---------------------------------------------------------------- K5 LBVH
+@pytest.mark.parametrize("name", ["single", "small", "q150", "c1"])
+def test_bvh_invariants(G, name):
+    from paper_2509_07782_b200 import spatial
+
+    s = gscene(G, name)
+    boxes, children, parents = spatial.bvh_export(s)
+    n = s.n
+    lo64, hi64 = s.aabb_lo, s.aabb_hi
+    leaves = []
+    for i in range(max(n - 1, 1)):
+        for k in range(2):
+            c = int(children[i, k])
+            if c == -(1 << 31):
+                continue
+            blo, bhi = boxes[i, k, 0].astype(np.float64), boxes[i, k, 1].astype(np.float64)
+            if c < 0:
+                p = ~c
+                leaves.append(p)
+                assert np.all(blo <= lo64[p]) and np.all(bhi >= hi64[p])
+            else:
+                assert 0 < c < n - 1
+                clo = np.minimum(boxes[c, 0, 0], boxes[c, 1, 0])
+                chi = np.maximum(boxes[c, 0, 1], boxes[c, 1, 1])
+                assert np.all(blo <= clo) and np.all(bhi >= chi)
+    assert sorted(leaves) == list(range(n))
+
+
+# ---------------------------------------------------------------- K10 queries
+def test_collect_sets_bit_exact(G):
+    from paper_2509_07782_b200 import spatial
+
+    g = golden("queries")
+    s = gscene(G, "q150")
+    Q, offs, sets = g["q150.queries"], g["q150.offsets"], g["q150.sets"]
+    counts, idx, st = spatial.collect_segments(s, Q, capacity=256)
+    for i in range(len(Q)):
+        want = sets[offs[i]:offs[i + 1]]
+        assert counts[i] == len(want)
+        assert np.array_equal(idx[i, :counts[i]], want), i
+
+
+def test_collect_brute_force_c1(G, rng):
+    from paper_2509_07782_b200 import spatial
+
+    s = gscene(G, "c1")
+    o_s = O.OracleScene(f32_records(gen_test_scene_records(**SPECS["c1"])))
+    Q = []
+    for _ in range(500):
+        o = rng.uniform(-2, 2, 3)
+        d = rng.standard_normal(3)
+        d /= np.linalg.norm(d)
+        t0 = rng.uniform(0, 3)
+        Q.append(np.concatenate([o, d, [t0, t0 + rng.uniform(0, 0.5)]]))
+    Q = np.array(Q)
+    counts, idx, st = spatial.collect_segments(s, Q, capacity=512)
+    for i, q in enumerate(Q):
+        want = o_s.segment_overlaps_brute(q[:3], q[3:6], q[6], q[7])
+        assert np.array_equal(idx[i, :counts[i]], want)
+
+
+def test_collect_overflow(G):
+    from paper_2509_07782_b200 import spatial
+
+    s = gscene(G, "q150")
+    with pytest.raises(G.BufferOverflow):
+        spatial.segment_overlaps(s, [-3.0, 0, 0], [1.0, 0, 0], 0.0, 8.0, capacity=1)
+    # enclosed segment and empty region (test_spatial.py:186-199)
+    one = gscene(G, "single")
+    assert list(spatial.segment_overlaps(one, np.zeros(3), [1.0, 0, 0], 0.0, 1e-4)) == [0]
+    assert len(spatial.segment_overlaps(gscene(G, "q150"), [0.0, 0, 50.0], [1.0, 0, 0], 0.0,
+                                        1.0)) == 0
+
+
+@pytest.mark.parametrize("name", ["q100", "q30"])
+def test_closest_hit(G, name):
+    from paper_2509_07782_b200 import spatial
+
+    g = golden("queries")
+    s = gscene(G, name)
+    got = spatial.closest_hits(s, g[f"{name}.queries"])
+    want = g[f"{name}.hits"]
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert np.max(np.abs(got[ok] - want[ok])) < 1e-9
+
+
+def test_closest_hit_known(G):
+    from paper_2509_07782_b200 import spatial
+
+    one = gscene(G, "single")
+    assert spatial.closest_hit(one, np.zeros(3), [1.0, 0, 0], 0.0, 10.0) == 0.0
+    assert spatial.closest_hit(gscene(G, "q150"), [0.0, 0, 50.0], [1.0, 0, 0], 0.0, 100.0) is None
+
+
+# ---------------------------------------------------------------- K6 forward render
+@pytest.mark.parametrize("scene,cname", [("small", c) for c in CFG] +
+                         [(s, c) for s in ("grid", "shell", "single") for c in ("uniform", "adaptive")])
+def test_render_small_vs_reference(G, scene, cname):
+    g = golden("render_small")
+    cam = camera_from(G, g, "cam16")
+    cfg = G.RenderConfig(**CFG[cname])
+    rgb, depth, trans, stats = G.render_full(gscene(G, scene), cam, cfg)
+    assert np.max(np.abs(rgb - g[f"{scene}.{cname}.rgb"])) < RGB_TOL
+    assert np.max(np.abs(trans - g[f"{scene}.{cname}.T"])) < T_TOL
+    # depth against the oracle (the reference has no depth output)
+    os_ = O.OracleScene(f32_records(gen_test_scene_records(**SPECS[scene])))
+    rays = O.camera_rays(cam.center, cam.quat, cam.focal, cam.width, cam.height)
+    _, _, D, _ = os_.render(rays, cam.height, cam.width, O.OCfg.make(**CFG[cname]))
+    tf = np.nan_to_num(g[f"{scene}.{cname}.rays"][..., 7], nan=1.0)
+    assert np.all(np.abs(depth - D) <= 1e-4 * np.maximum(tf, 1.0))
+    ref = g[f"{scene}.{cname}.stats"]
+    got = [stats.rays, stats.samples, stats.segments, stats.segments_skipped,
+           stats.closest_hit_calls]
+    if cname != "uniform_bg_cap2":  # the reference counts overflow sub-segments
+        assert got == list(ref[:5])
+        assert stats.aabb_hits == ref[6] and stats.ellipsoid_hits == ref[7]
+
+
+def test_render_camera_b(G):
+    g = golden("render_small")
+    cam = camera_from(G, g, "camb")
+    for cname in ("uniform", "adaptive"):
+        rgb, depth, trans, _ = G.render_full(gscene(G, "q150"), cam, G.RenderConfig(**CFG[cname]))
+        assert np.max(np.abs(rgb - g[f"q150.{cname}.rgb"])) < RGB_TOL
+        assert np.max(np.abs(trans - g[f"q150.{cname}.T"])) < T_TOL
+
+
+def test_render_c1_full_frame(G):
+    g = golden("render_c1")
+    cam = camera_from(G, g, "cam64")
+    rgb, depth, trans, st = G.render_full(gscene(G, "c1"), cam, G.RenderConfig())
+    assert np.max(np.abs(rgb - g["c1.uniform.rgb"])) < RGB_TOL
+    assert np.max(np.abs(trans - g["c1.uniform.T"])) < T_TOL
+    ref = g["c1.uniform.stats6"]
+    assert [st.samples, st.segments, st.segments_skipped, st.closest_hit_calls, st.aabb_hits,
+            st.ellipsoid_hits] == list(ref)
+
+
+def test_render_c1_adaptive(G):
+    g = golden("render_c1")
+    cam = camera_from(G, g, "cam64")
+    rgb, depth, trans, st = G.render_full(gscene(G, "c1"), cam, G.RenderConfig(mode="adaptive"))
+    assert np.max(np.abs(rgb[::4, ::4] - g["c1.adaptive_sub4.rgb"])) < RGB_TOL
+    assert np.max(np.abs(trans[::4, ::4] - g["c1.adaptive_sub4.T"])) < T_TOL
+
+
+def test_render_c1_vs_oracle_all_outputs(G):
+    """Full-frame adaptive + uniform vs the oracle, including depth."""
+    g = golden("render_c1")
+    cam = camera_from(G, g, "cam64")
+    os_ = O.OracleScene(f32_records(gen_test_scene_records(**SPECS["c1"])))
+    rays = O.camera_rays(cam.center, cam.quat, cam.focal, 64, 64)
+    for mode in ("uniform", "adaptive"):
+        rgb, depth, trans, _ = G.render_full(gscene(G, "c1"), cam, G.RenderConfig(mode=mode))
+        R, T, D, _ = os_.render(rays, 64, 64, O.OCfg.make(mode=mode), threads=8)
+        assert np.max(np.abs(rgb - R)) < RGB_TOL, mode
+        assert np.max(np.abs(trans - T)) < T_TOL, mode
+        assert np.max(np.abs(depth - D)) < 1e-4 * 5.0, mode
+
+
+def test_ess_and_tiles_invariance(G):
+    g = golden("render_small")
+    cam = camera_from(G, g, "cam16")
+    s = gscene(G, "small")
+    a = G.render_full(s, cam, G.RenderConfig(ess=True))[0]
+    b = G.render_full(s, cam, G.RenderConfig(ess=False))[0]
+    assert np.max(np.abs(a - b)) < 1e-6
+    # tile sharding (multi-GPU layout): two disjoint tile sets == full frame
+    import torch
+
+    cam64 = camera_from(G, golden("render_c1"), "cam64")
+    c1 = gscene(G, "c1")
+    full = G.render(c1, cam64, G.RenderConfig())[0].cpu().numpy()
+    rgb = torch.full((64, 64, 3), -1.0, device="cuda")
+    G.render(c1, cam64, G.RenderConfig(), tile_begin=0, tile_stride=2, rgb=rgb)
+    G.render(c1, cam64, G.RenderConfig(), tile_begin=1, tile_stride=2, rgb=rgb)
+    assert np.array_equal(rgb.cpu().numpy(), full)
+
+
+def test_morton_invariance(G):
+    g = golden("render_small")
+    cam = camera_from(G, g, "cam16")
+    a = G.Scene.from_records(f32_records(gen_test_scene_records(**SPECS["small"])))
+    b = G.Scene.from_records(f32_records(gen_test_scene_records(**SPECS["small"])))
+    G.reorder_by_morton(b)
+    ia = G.render_full(a, cam, G.RenderConfig())[0]
+    ib = G.render_full(b, cam, G.RenderConfig())[0]
+    assert np.max(np.abs(ia - ib)) < 1e-6
+
+
+def test_transmittance_closed_form(G):
+    # test_renderer.py:125-138: sigma_eps = 1e-8, line integral 2*0.3*sqrt(2 pi)
+    import math
+
+    rec = np.zeros((1, 87))
+    rec[0, 3] = 1.0
+    rec[0, 7:10] = 0.3
+    rec[0, 10] = 2.0
+    rec[0, 11:14] = np.array([1.0, 1.0, 1.0]) / 0.28209479177387814
+    rec[0, 38:59] = np.tile([0.0, 0.0, 1.0], 7)
+    s = G.Scene.from_records(rec, sigma_eps=1e-8)
+    ray = G.clip_ray_to_scene(s, G.Ray([0, 0, -5], [0, 0, 1], 1e-4, 1e6))
+    _, st = G.march_ray(s, ray, G.RenderConfig(dt=0.0005, ess=False))
+    assert st.transmittance == pytest.approx(math.exp(-2.0 * 0.3 * math.sqrt(2 * math.pi)),
+                                             abs=1e-4)
+
+
+def test_background_passthrough(G):
+    s = gscene(G, "single")
+    rgb, st = G.march_ray(s, G.Ray([0, 0, -5], [0, 1, 0], 0.0, 1.0),
+                          G.RenderConfig(background=(0.1, 0.2, 0.3)))
+    assert np.allclose(rgb, [0.1, 0.2, 0.3], atol=1e-7)
+    assert st.transmittance == 1.0
+
+
+def test_march_rays_vs_oracle(G, rng):
+    """Explicit rays (march_ray semantics, no clipping) incl. origins inside."""
+    s = gscene(G, "q150")
+    os_ = O.OracleScene(f32_records(gen_test_scene_records(**SPECS["q150"])))
+    rays = []
+    for _ in range(300):
+        o = rng.uniform(-1.2, 1.2, 3)
+        d = rng.standard_normal(3)
+        d /= np.linalg.norm(d)
+        rays.append(np.concatenate([o, d, [1e-4, rng.uniform(0.5, 4.0)]]))
+    rays = np.array(rays)
+    for mode in ("uniform", "adaptive"):
+        cfg = G.RenderConfig(mode=mode)
+        rgb, depth, trans, st = G.march_rays(s, rays, cfg, clip=False, stats=True)
+        R, T, D, ost = os_.march_rays(rays, O.OCfg.make(mode=mode), clip=False)
+        assert np.max(np.abs(rgb - R)) < RGB_TOL, mode
+        assert np.max(np.abs(trans - T)) < T_TOL, mode
+        assert np.max(np.abs(depth - D)) < 1e-4 * 4.0, mode
+        assert st.samples == ost["samples"] and st.aabb_hits == ost["aabb_hits"], mode
+
+
+def test_config_validation(G):
+    with pytest.raises(ValueError):
+        G.RenderConfig(mode="fancy")
+    with pytest.raises(ValueError):
+        G.RenderConfig(t_eps=0.0)
+    with pytest.raises(ValueError):
+        G.RenderConfig(dt_min=0.1, dt_max=0.01)
