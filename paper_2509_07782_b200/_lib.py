@@ -110,7 +110,7 @@ def load_library(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("GSX_LIB", LIB_PATH))
     if not p.exists():
         raise GsxUnavailable(f"{p} not built; run __graft_entry__.build() (nvcc, sm_100a)")
     L = ctypes.CDLL(str(p))

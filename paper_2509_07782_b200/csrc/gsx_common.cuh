@@ -16,7 +16,7 @@
 //   aabb64 : double[n][6]  lo xyz, hi xyz   (scene.py:61-65, exact fp64)
 //   inv64  : double[n][9]  iso_inv          (scene.py:58-60, exact fp64)
 //   lr64   : double[n]     log_ratio        (scene.py:55)
-//   geo    : float4[n][4]  (mu, sigma~) (M row0, k*log2e/2) (M row1, 0) (M row2, 0)
+//   geo    : float4[n][4]  (mu, sigma~) (M row0, k*log2e/2) (M row1, k) (M row2, log2 sigma~)
 //   box32  : float[n][6]   outward-rounded fp32 AABB (LBVH leaves)
 //   app    : float4[n][19] sh 27 | unit sg axes 21 | sharpness 7 | amp 21
 //   bounds : double[6]     scene AABB lo xyz, hi xyz (scene.py:66-67)
@@ -24,6 +24,8 @@
 // ---------------------------------------------------------------------------
 #define GSX_BOUNDS_BLOCKS 296
 
+//   gaux   : float4[n][5]  backward helpers: (unit quat w,x,y,z) (1/|q_raw|, s clamped xyz)
+//            (sqrt k, scale-not-clamped mask xyz) (1/|axis_raw| lobes 0..3) (lobes 4..6, 0)
 struct SceneView {
   double* aabb64;
   double* inv64;
@@ -33,6 +35,7 @@ struct SceneView {
   float4* app;
   double* bounds;
   double* part;
+  float4* gaux;
 };
 
 static inline size_t gsx_align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -50,7 +53,8 @@ __host__ __device__ inline SceneView scene_view(void* arena, int64_t n) {
   v.box32 = (float*)(p + off);   off += gsx_al(sizeof(float) * 6 * n);
   v.app = (float4*)(p + off);    off += gsx_al(sizeof(float4) * 19 * n);
   v.bounds = (double*)(p + off); off += gsx_al(sizeof(double) * 6);
-  v.part = (double*)(p + off);
+  v.part = (double*)(p + off);   off += gsx_al(sizeof(double) * 6 * GSX_BOUNDS_BLOCKS);
+  v.gaux = (float4*)(p + off);
   return v;
 }
 
@@ -64,6 +68,7 @@ inline size_t scene_arena_bytes_impl(int64_t n) {
   s += gsx_align256(sizeof(float4) * 19 * n);
   s += gsx_align256(sizeof(double) * 6);
   s += gsx_align256(sizeof(double) * 6 * GSX_BOUNDS_BLOCKS);
+  s += gsx_align256(sizeof(float4) * 5 * n);
   return s;
 }
 
@@ -74,10 +79,19 @@ inline size_t scene_arena_bytes_impl(int64_t n) {
 // child >= 0: internal node index; child < 0: leaf ~prim; GSX_NONE: absent.
 // parents int32[2n-1] (internal 0..n-2, leaf i at n-1+i).  Root = node 0.
 // For n == 1 a single node holds leaf 0 on the left and GSX_NONE on the right.
+//
+// 4-wide collapse (used by the warp-cooperative packet traversal): the binary
+// internal nodes at even depth are kept, odd-depth ones are absorbed into their
+// parent, so every 4-wide node holds up to 4 children (grandchildren of the
+// binary node).  Node = float4[8] (128 B):
+//   q0 = lo.x[4]  q1 = lo.y[4]  q2 = lo.z[4]  q3 = hi.x[4]  q4 = hi.y[4]
+//   q5 = hi.z[4]  q6 = child[4] (int bits, same encoding)  q7 = unused
+// Root = node 0.
 // ---------------------------------------------------------------------------
 struct BvhView {
   float4* nodes;
   int32_t* parents;
+  float4* nodes4;
 };
 
 __host__ __device__ inline int64_t bvh_internal_count(int64_t n) { return n > 1 ? n - 1 : 1; }
@@ -86,15 +100,22 @@ __host__ __device__ inline BvhView bvh_view(void* arena, int64_t n) {
   char* p = (char*)arena;
   BvhView v;
   size_t a = ((sizeof(float4) * 4 * bvh_internal_count(n)) + 255) & ~(size_t)255;
+  size_t b = ((sizeof(int32_t) * (2 * n + 1)) + 255) & ~(size_t)255;
   v.nodes = (float4*)p;
   v.parents = (int32_t*)(p + a);
+  v.nodes4 = (float4*)(p + a + b);
   return v;
 }
 
 inline size_t bvh_arena_bytes_impl(int64_t n) {
   return gsx_align256(sizeof(float4) * 4 * bvh_internal_count(n)) +
-         gsx_align256(sizeof(int32_t) * (2 * n + 1));
+         gsx_align256(sizeof(int32_t) * (2 * n + 1)) +
+         gsx_align256(sizeof(float4) * 8 * bvh_internal_count(n));
 }
+
+// device-wide exclusive scan of u32 (morton_sort.cu); sums: scan workspace
+size_t gsx_scan_ws_elems(int64_t len);
+void gsx_exclusive_scan_u32(uint32_t* data, int64_t len, uint32_t* sums, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // device status helpers
@@ -199,3 +220,4 @@ __device__ inline int32_t f_as_i(float f) { return __float_as_int(f); }
 
 void gsx_set_cuda_error(cudaError_t e);
 int gsx_check_launch();
+int gsx_validate_cfg(const gsx_render_cfg* cfg);

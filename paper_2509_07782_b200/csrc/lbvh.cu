@@ -100,7 +100,8 @@ __global__ void k_refit(const float* __restrict__ box32, int64_t n, float4* node
   }
 }
 
-__global__ void k_single(const float* __restrict__ box32, float4* nodes, int32_t* parents) {
+__global__ void k_single(const float* __restrict__ box32, float4* nodes, int32_t* parents,
+                         float4* nodes4) {
   Box b = leaf_box(box32, 0);
   nodes[0] = make_float4(b.lo[0], b.lo[1], b.lo[2], __int_as_float(~0));
   nodes[1] = make_float4(b.hi[0], b.hi[1], b.hi[2], __int_as_float(GSX_NONE));
@@ -108,6 +109,76 @@ __global__ void k_single(const float* __restrict__ box32, float4* nodes, int32_t
   nodes[3] = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
   parents[0] = -1;
   parents[1] = 0;  // leaf 0 (slot n-1+0 == 0 would collide; n==1 uses slot 1)
+  float inf = INFINITY;
+  nodes4[0] = make_float4(b.lo[0], inf, inf, inf);
+  nodes4[1] = make_float4(b.lo[1], inf, inf, inf);
+  nodes4[2] = make_float4(b.lo[2], inf, inf, inf);
+  nodes4[3] = make_float4(b.hi[0], -inf, -inf, -inf);
+  nodes4[4] = make_float4(b.hi[1], -inf, -inf, -inf);
+  nodes4[5] = make_float4(b.hi[2], -inf, -inf, -inf);
+  int none = GSX_NONE;
+  nodes4[6] = make_float4(__int_as_float(~0), __int_as_float(none), __int_as_float(none),
+                          __int_as_float(none));
+  nodes4[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// ---- 4-wide collapse ----------------------------------------------------------
+// keep[i] = 1 for binary internal nodes at even depth (root included)
+__global__ void k_keep_flags(const int32_t* __restrict__ parents, int64_t n, uint32_t* keep) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = 0;
+  for (int32_t p = parents[i]; p >= 0; p = parents[p]) ++d;
+  keep[i] = (d & 1) ? 0u : 1u;
+}
+
+__global__ void k_collapse(const float4* __restrict__ nodes, const uint32_t* __restrict__ keep,
+                           const uint32_t* __restrict__ idx4, int64_t n, float4* nodes4) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1 || !keep[i]) return;
+  float lo[3][4], hi[3][4];
+  int32_t ch[4];
+  int cnt = 0;
+  auto add = [&](const float4& l, const float4& h, int32_t c) {
+    lo[0][cnt] = l.x; lo[1][cnt] = l.y; lo[2][cnt] = l.z;
+    hi[0][cnt] = h.x; hi[1][cnt] = h.y; hi[2][cnt] = h.z;
+    ch[cnt++] = c;
+  };
+  const float4* nd = nodes + 4 * i;
+  float4 q[4] = {nd[0], nd[1], nd[2], nd[3]};
+  int32_t bc[2] = {__float_as_int(q[0].w), __float_as_int(q[1].w)};
+  for (int k = 0; k < 2; ++k) {
+    int32_t c = bc[k];
+    if (c == GSX_NONE) continue;
+    if (c < 0) {
+      add(q[2 * k], q[2 * k + 1], c);
+      continue;
+    }
+    // absorbed odd-depth node: take its two children
+    const float4* cd = nodes + 4 * (int64_t)c;
+    float4 r[4] = {cd[0], cd[1], cd[2], cd[3]};
+    int32_t gc[2] = {__float_as_int(r[0].w), __float_as_int(r[1].w)};
+    for (int m = 0; m < 2; ++m) {
+      int32_t g = gc[m];
+      if (g == GSX_NONE) continue;
+      add(r[2 * m], r[2 * m + 1], g < 0 ? g : (int32_t)idx4[g]);
+    }
+  }
+  for (; cnt < 4;) {
+    lo[0][cnt] = lo[1][cnt] = lo[2][cnt] = INFINITY;
+    hi[0][cnt] = hi[1][cnt] = hi[2][cnt] = -INFINITY;
+    ch[cnt++] = GSX_NONE;
+  }
+  float4* o = nodes4 + 8 * (int64_t)idx4[i];
+  o[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+  o[1] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+  o[2] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+  o[3] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+  o[4] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+  o[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+  o[6] = make_float4(__int_as_float(ch[0]), __int_as_float(ch[1]), __int_as_float(ch[2]),
+                     __int_as_float(ch[3]));
+  o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* children) {
@@ -126,7 +197,8 @@ __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* 
 
 extern "C" size_t gsx_bvh_arena_bytes(int64_t n) { return bvh_arena_bytes_impl(n); }
 extern "C" size_t gsx_bvh_workspace_bytes(int64_t n) {
-  return gsx_align256(sizeof(int32_t) * (n > 1 ? n : 1));
+  int64_t m = n > 1 ? n : 1;
+  return 3 * gsx_align256(sizeof(int32_t) * m) + gsx_align256(sizeof(uint32_t) * gsx_scan_ws_elems(m));
 }
 
 extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_codes,
@@ -138,14 +210,24 @@ extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_cod
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view(bvh_arena, n);
   if (n == 1) {
-    k_single<<<1, 1, 0, s>>>(sv.box32, bv.nodes, bv.parents);
+    k_single<<<1, 1, 0, s>>>(sv.box32, bv.nodes, bv.parents, bv.nodes4);
     return gsx_check_launch();
   }
-  int32_t* flags = (int32_t*)workspace;
+  char* w = (char*)workspace;
+  size_t seg = gsx_align256(sizeof(int32_t) * n);
+  int32_t* flags = (int32_t*)w;
+  uint32_t* keep = (uint32_t*)(w + seg);
+  uint32_t* idx4 = (uint32_t*)(w + 2 * seg);
+  uint32_t* sums = (uint32_t*)(w + 3 * seg);
   CUDA_CHECK_RET(cudaMemsetAsync(flags, 0, sizeof(int32_t) * (n - 1), s));
-  k_karras<<<(unsigned)((n - 1 + 255) / 256), 256, 0, s>>>(sorted_codes, perm, n, bv.nodes,
-                                                           bv.parents);
+  unsigned gi = (unsigned)((n - 1 + 255) / 256);
+  k_karras<<<gi, 256, 0, s>>>(sorted_codes, perm, n, bv.nodes, bv.parents);
   k_refit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sv.box32, n, bv.nodes, bv.parents, flags);
+  // 4-wide collapse for the packet traversal
+  k_keep_flags<<<gi, 256, 0, s>>>(bv.parents, n, keep);
+  CUDA_CHECK_RET(cudaMemcpyAsync(idx4, keep, sizeof(uint32_t) * (n - 1), cudaMemcpyDeviceToDevice, s));
+  gsx_exclusive_scan_u32(idx4, n - 1, sums, s);
+  k_collapse<<<gi, 256, 0, s>>>(bv.nodes, keep, idx4, n, bv.nodes4);
   return gsx_check_launch();
 }
 

@@ -401,3 +401,13 @@ extern "C" int gsx_permute(const float* params, const int64_t* uids_in, const in
     k_permute_uids<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(uids_in, perm, n, uids_out);
   return gsx_check_launch();
 }
+
+size_t gsx_scan_ws_elems(int64_t len) { return (size_t)scan_blocks(len) + 1; }
+
+void gsx_exclusive_scan_u32(uint32_t* data, int64_t len, uint32_t* sums, cudaStream_t s) {
+  if (len <= 0) return;
+  int sb = scan_blocks(len);
+  k_scan_tiles<<<sb, SCAN_THREADS, 0, s>>>(data, len, sums);
+  k_scan_sums<<<1, SCAN_THREADS, 0, s>>>(sums, sb);
+  k_scan_add<<<sb, SCAN_THREADS, 0, s>>>(data, len, sums);
+}

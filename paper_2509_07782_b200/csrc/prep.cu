@@ -95,7 +95,7 @@ __global__ void k_prepare(const float* __restrict__ params, int64_t n, double si
   g[0] = make_float4(r[0], r[1], r[2], r[10]);
   g[1] = make_float4((float)M[0], (float)M[1], (float)M[2], (float)(0.5 * lr * LOG2E));
   g[2] = make_float4((float)M[3], (float)M[4], (float)M[5], (float)lr);
-  g[3] = make_float4((float)M[6], (float)M[7], (float)M[8], 0.f);
+  g[3] = make_float4((float)M[6], (float)M[7], (float)M[8], (float)log2(sigma));
   float* b32 = v.box32 + 6 * i;
   for (int k = 0; k < 3; ++k) {
     b32[k] = __double2float_rd(lo[k]);
@@ -109,6 +109,19 @@ __global__ void k_prepare(const float* __restrict__ params, int64_t n, double si
   for (int k = 0; k < 21; ++k) a[55 + k] = r[66 + k];
   float4* ap = v.app + 19 * i;
   for (int k = 0; k < 19; ++k) ap[k] = make_float4(a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
+  // backward helpers (render_bwd.cu)
+  float ian[7];
+  for (int l = 0; l < 7; ++l) {
+    double ax[3] = {(double)r[38 + 3 * l], (double)r[39 + 3 * l], (double)r[40 + 3 * l]};
+    ian[l] = (float)(1.0 / norm3(ax));
+  }
+  float4* ga = v.gaux + 5 * i;
+  ga[0] = make_float4((float)w, (float)x, (float)y, (float)z);
+  ga[1] = make_float4((float)(1.0 / qn), (float)sc[0], (float)sc[1], (float)sc[2]);
+  ga[2] = make_float4((float)sq, (double)r[7] > 1e-7 ? 1.f : 0.f, (double)r[8] > 1e-7 ? 1.f : 0.f,
+                      (double)r[9] > 1e-7 ? 1.f : 0.f);
+  ga[3] = make_float4(ian[0], ian[1], ian[2], ian[3]);
+  ga[4] = make_float4(ian[4], ian[5], ian[6], 0.f);
 }
 
 // scene bounds: min/max over AABBs (exact; order independent)

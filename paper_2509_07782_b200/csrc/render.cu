@@ -4,208 +4,80 @@
 // appearance.py:91-98).
 //
 // One thread per ray; a CTA renders one 16x16 tile with pixels in Z-order
-// (each warp = an 8x4 pixel block).  Per segment ("slab by slab") the thread
-// traverses the LBVH with fp32 slab tests (conservative margin) and processes
-// each candidate immediately: an fp64 per-(ray, primitive) setup reduces the
-// density along the ray to q(t) = A (t - t_c)^2 + q_min, then the 16 samples
-// of the segment are accumulated in registers with one FMA pair + one EX2 per
-// (sample, primitive).  AABB-emptiness (which drives empty-space skipping) is
-// decided with the reference's exact fp64 slab test on the candidates, so ESS
-// jumps and adaptive grid restarts happen exactly where the reference's do.
+// (each warp = an 8x4 pixel block, so its 32 rays are spatially coherent).
+// The warp marches in lockstep, one segment per lane per iteration ("slab by
+// slab", render_warp.cuh): a warp-cooperative traversal of the 4-wide BVH
+// over the union of the 32 segments (fp32 slab tests, conservative margin)
+// stages the candidates in a shared-memory list; every lane then evaluates
+// the list against its own ray: an fp32 per-(ray, primitive) setup relative
+// to the segment's base point reduces the density along the ray to
+// q(t) = A (t - t_c)^2 + q_min, and the 16 samples of the segment accumulate
+// in registers with one FMA pair + one EX2 per (sample, primitive).
+// AABB-emptiness (which drives empty-space skipping) is decided with the
+// reference's exact fp64 slab test on the candidates, so ESS jumps and
+// adaptive grid restarts happen exactly where the reference's do.
 #include "gsx_common.cuh"
-#include "render_common.cuh"
+#include "render_warp.cuh"
+
+#ifdef GSX_PHASE_PROF
+namespace gsx {
+__device__ unsigned long long g_phase[16];
+}
+#endif
 
 namespace {
 
 using namespace gsx;
 
+// One warp iteration over a segment (all 32 lanes; lanes with want == false
+// only help traversing).  Accumulates and composites the lane's samples and
+// returns its exact AABB-emptiness verdict.
 template <bool STATS>
-struct Counters {
-  uint32_t samples = 0, segments = 0, skipped = 0, ch_calls = 0, visits = 0, aabb = 0, ell = 0,
-           pairs = 0, composited = 0;
-};
-
-// Process the samples of one segment (or one 16-sample chunk of it):
-// traverse [t0, t1], accumulate sigma/W for samples tbase + j*dt (j < m),
-// composite them.  Returns whether any AABB exactly overlaps [t0, t1].
-template <bool STATS>
-__device__ bool segment_pass(const SceneView& sv, const BvhView& bv, const RayCtx& r, double t0,
-                             double t1, double tbase, double dt, int m, const float Y[9],
-                             RayAccum& acc, Counters<STATS>& cnt) {
-  float sig[16];
-  float W[16][3];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    sig[j] = 0.f;
-    W[j][0] = W[j][1] = W[j][2] = 0.f;
-  }
+__device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+                                bool want, const Seg& seg, int ns, const float* Y,
+                                RayAccum& acc, Counters<STATS>& cnt, WarpSmem& sm) {
   bool nonempty = false;
-  const float dtf = (float)dt;
-  auto leaf = [&](int64_t p) {
-    if (STATS || !nonempty) {
-      if (exact_aabb_overlap(sv, r, p, t0, t1)) {
-        nonempty = true;
-        if (STATS) {
-          cnt.aabb++;
-          if (ellipsoid_hits_interval(sv, r, p, t0, t1)) cnt.ell++;
-        }
-      }
-    }
-    if (m <= 0) return;
-    CandSetup cs;
-    if (!cand_setup(sv, r, p, tbase, cs)) return;
-    int jlo, jhi;
-    if (!sample_range(cs, dtf, m, jlo, jhi)) return;
-    float c[3];
-    eval_radiance_f(sv.app + 19 * p, Y, r.df, c);
+  const float dtf = (float)seg.dt;
+  const SegLimits lim = seg_limits(r, seg);
+  const int nchunks = (ns + 15) / 16;
+  uint32_t visits = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int mc = want ? seg.m - ch * 16 : 0;
+    mc = mc < 0 ? 0 : (mc > 16 ? 16 : mc);
+    const double tb = seg.tbase + (double)(ch * 16) * seg.dt;
+    const SegBase base = seg_base(r, tb);
+    float sig[16];
+    float W[16][3];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      if (j >= jlo && j <= jhi) {
-        float del = fmaf((float)j, dtf, cs.del0);
-        float q = fmaf(cs.A * del, del, cs.qmin);
-        if (q <= 1.0f) {
-          float dens = cs.sigma * ex2_approx(-cs.kl2 * q);
-          sig[j] += dens;
-          W[j][0] = fmaf(dens, c[0], W[j][0]);
-          W[j][1] = fmaf(dens, c[1], W[j][1]);
-          W[j][2] = fmaf(dens, c[2], W[j][2]);
-        }
-      }
+      sig[j] = 0.f;
+      W[j][0] = W[j][1] = W[j][2] = 0.f;
     }
-  };
-  uint32_t visits = 0;
-  uint32_t aabb_before = cnt.aabb;
-  bool ok = traverse_segment(bv, r, (float)t0, (float)t1, leaf, visits);
-  (void)ok;
-  if (STATS) {
-    cnt.visits += visits;
-    cnt.pairs += (uint32_t)m * (cnt.aabb - aabb_before);
+    if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
+    for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, visits, [&](int64_t p) {
+      if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
+        nonempty = true;
+      accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
+    });
+    if (STATS) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) cnt.composited += (j < m && sig[j] > 0.f) ? 1u : 0u;
-  }
-  // front-to-back compositing (renderer.py:230-239)
+      for (int j = 0; j < 16; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
+    }
+    PH_BEGIN(ph_c)
+    // front-to-back compositing (renderer.py:230-239); zero-density samples
+    // leave the state unchanged, so compositing an empty segment is a no-op
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < m) {
-      float tj = (float)(tbase + (double)j * dt);
-      acc.add_sample(sig[j], W[j], tj, dtf);
+    for (int j = 0; j < 16; ++j) {
+      if (j < mc) {
+        float tj = (float)(tb + (double)j * seg.dt);
+        acc.add_sample(sig[j], W[j], tj, dtf);
+      }
     }
+    PH_END(3, ph_c)
   }
-  return nonempty;
-}
-
-template <bool STATS>
-__device__ bool process_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
-                                const gsx_render_cfg& cfg, double t0, double t1, double tbase,
-                                double dt, int m, const float Y[9], RayAccum& acc,
-                                Counters<STATS>& cnt) {
-  int ns = (int)cfg.n_s;
-  bool nonempty = false;
-  for (int c = 0; c * 16 < ns || c == 0; ++c) {
-    int mc = m - c * 16;
-    mc = mc < 0 ? 0 : (mc > 16 ? 16 : mc);
-    if (c > 0 && mc == 0 && nonempty) break;
-    bool ne = segment_pass<STATS>(sv, bv, r, t0, t1, tbase + (double)(c * 16) * dt, dt, mc, Y,
-                                  acc, cnt);
-    nonempty |= ne;
-  }
-  return nonempty;
-}
-
-template <bool STATS>
-__device__ void march(const SceneView& sv, const BvhView& bv, const RayCtx& r,
-                      const gsx_render_cfg& cfg, RayAccum& acc, Counters<STATS>& cnt) {
-  float Y[9];
-  sh_basis_f(r.df, Y);
-  const double t_n = r.t_n, t_f = r.t_f;
-  const int ns = (int)cfg.n_s;
-  uint32_t visits = 0;
-  if (cfg.mode == 0) {
-    // _march_uniform (renderer.py:288-323)
-    const double ds = cfg.dt * (double)ns;
-    long long n_seg = (long long)ceil((t_f - t_n) / ds);
-    if (n_seg < 1) n_seg = 1;
-    long long k = 0;
-    if (cfg.ess) {
-      double hit;
-      if (STATS) cnt.ch_calls++;
-      bool found = closest_hit_r(sv, bv, r, t_n, t_f, hit, visits);
-      if (!found) goto done;
-      long long kk = (long long)((hit - t_n) / ds);
-      k = kk > 0 ? kk : 0;
-    }
-    while (k < n_seg && acc.transmittance() > cfg.t_eps) {
-      double t0 = t_n + (double)k * ds;
-      double t1 = t0 + ds;
-      if (t_f < t1) t1 = t_f;
-      long long j0 = k * ns;
-      int m = 0;
-      for (int j = 0; j < ns; ++j)
-        if (t_n + ((double)(j0 + j) + 0.5) * cfg.dt < t_f) m = j + 1;
-      double tbase = t_n + ((double)j0 + 0.5) * cfg.dt;
-      bool ne = process_segment<STATS>(sv, bv, r, cfg, t0, t1, tbase, cfg.dt, m, Y, acc, cnt);
-      if (!ne) {
-        if (STATS) cnt.skipped++;
-        if (cfg.ess) {
-          double hit;
-          if (STATS) cnt.ch_calls++;
-          if (!closest_hit_r(sv, bv, r, t1, t_f, hit, visits)) break;
-          long long kk = (long long)((hit - t_n) / ds);
-          k = kk > k + 1 ? kk : k + 1;
-        } else {
-          if (STATS) cnt.samples += m;
-          k += 1;
-        }
-        continue;
-      }
-      if (STATS) {
-        cnt.segments++;
-        cnt.samples += m;
-      }
-      k += 1;
-    }
-  } else {
-    // _march_adaptive (renderer.py:326-358)
-    double t_s = t_n;
-    if (cfg.ess) {
-      double hit;
-      if (STATS) cnt.ch_calls++;
-      if (!closest_hit_r(sv, bv, r, t_n, t_f, hit, visits)) goto done;
-      t_s = hit;
-    }
-    while (t_s < t_f && acc.transmittance() > cfg.t_eps) {
-      double T = (double)acc.transmittance();
-      double ds = segment_step(cfg, t_s, T);
-      double dt = ds / (double)ns;
-      double t1 = t_s + ds;
-      if (t_f < t1) t1 = t_f;
-      int m = 0;
-      for (int j = 0; j < ns; ++j)
-        if (t_s + ((double)j + 0.5) * dt < t_f) m = j + 1;
-      double tbase = t_s + 0.5 * dt;
-      bool ne = process_segment<STATS>(sv, bv, r, cfg, t_s, t1, tbase, dt, m, Y, acc, cnt);
-      if (!ne) {
-        if (STATS) cnt.skipped++;
-        if (cfg.ess) {
-          double hit;
-          if (STATS) cnt.ch_calls++;
-          if (!closest_hit_r(sv, bv, r, t1, t_f, hit, visits)) break;
-          t_s = hit;
-        } else {
-          if (STATS) cnt.samples += m;
-          t_s = t_s + ds;
-        }
-        continue;
-      }
-      if (STATS) {
-        cnt.segments++;
-        cnt.samples += m;
-      }
-      t_s = t_s + ds;
-    }
-  }
-done:
   if (STATS) cnt.visits += visits;
+  emptiness_tail<STATS>(sv, bv, r, want, seg, nonempty, cnt);
+  return nonempty;
 }
 
 template <bool STATS>
@@ -222,11 +94,24 @@ __device__ void flush_stats(gsx_stats* st, const Counters<STATS>& c, bool is_ray
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_render_camera(SceneView sv, BvhView bv, gsx_camera cam,
-                                                       gsx_render_cfg cfg, int64_t tile_begin,
-                                                       int64_t tile_stride, float* rgb,
-                                                       float* depth, float* trans,
-                                                       gsx_stats* stats) {
+__device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayCtx& r, bool hit,
+                              const gsx_render_cfg& cfg, RayAccum& acc, Counters<STATS>& cnt,
+                              WarpSmem& sm) {
+  float Y[9];
+  sh_basis_f(r.df, Y);
+  const int ns = (int)cfg.n_s;
+  march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, [&](const Seg& seg, bool want) {
+    return forward_segment<STATS>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm);
+  });
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(256, 2) k_render_camera(SceneView sv, BvhView bv,
+                                                          gsx_camera cam, gsx_render_cfg cfg,
+                                                          int64_t tile_begin, int64_t tile_stride,
+                                                          float* rgb, float* depth, float* trans,
+                                                          gsx_stats* stats) {
+  __shared__ WarpSmem smem[8];
   int64_t W = cam.width, H = cam.height;
   int64_t tiles_x = (W + 15) / 16;
   int64_t tile = tile_begin + (int64_t)blockIdx.x * tile_stride;
@@ -235,15 +120,14 @@ __global__ void __launch_bounds__(256) k_render_camera(SceneView sv, BvhView bv,
   int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
   bool valid = px < W && py < H;
   Counters<STATS> cnt;
+  RayCtx r;
+  bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
+  RayAccum acc;
+  acc.init();
+  march_forward<STATS>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5]);
   if (valid) {
-    RayCtx r;
-    bool hit = camera_ray(cam, (double)px, (double)py, sv.bounds, r);
-    RayAccum acc;
-    acc.init();
-    if (hit) march<STATS>(sv, bv, r, cfg, acc, cnt);
     int64_t pix = py * W + px;
-    float T = acc.transmittance();
-    if (!hit) T = 1.f;
+    float T = hit ? acc.transmittance() : 1.f;
     for (int k = 0; k < 3; ++k) rgb[3 * pix + k] = acc.C[k] + T * (float)cfg.background[k];
     if (depth) depth[pix] = acc.D;
     if (trans) trans[pix] = T;
@@ -252,37 +136,27 @@ __global__ void __launch_bounds__(256) k_render_camera(SceneView sv, BvhView bv,
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(256) k_render_rays(SceneView sv, BvhView bv,
-                                                     const double* __restrict__ rays, int64_t m,
-                                                     int clip, gsx_render_cfg cfg, float* rgb,
-                                                     float* depth, float* trans,
-                                                     gsx_stats* stats) {
+__global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv,
+                                                        const double* __restrict__ rays,
+                                                        int64_t m, int clip, gsx_render_cfg cfg,
+                                                        float* rgb, float* depth, float* trans,
+                                                        gsx_stats* stats) {
+  __shared__ WarpSmem smem[8];
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = i < m;
   Counters<STATS> cnt;
+  RayCtx r;
+  bool hit = valid && explicit_ray(rays + 8 * i, clip != 0, sv.bounds, r);
+  RayAccum acc;
+  acc.init();
+  march_forward<STATS>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5]);
   if (valid) {
-    RayCtx r;
-    bool hit = explicit_ray(rays + 8 * i, clip != 0, sv.bounds, r);
-    RayAccum acc;
-    acc.init();
-    if (hit) march<STATS>(sv, bv, r, cfg, acc, cnt);
     float T = hit ? acc.transmittance() : 1.f;
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = acc.C[k] + T * (float)cfg.background[k];
     if (depth) depth[i] = acc.D;
     if (trans) trans[i] = T;
   }
   flush_stats<STATS>(stats, cnt, valid);
-}
-
-int validate_cfg(const gsx_render_cfg* cfg) {
-  // RenderConfig.__post_init__ (renderer.py:41-49)
-  if (!cfg) return GSX_ERR_ARG;
-  if (!(cfg->t_eps > 0.0 && cfg->t_eps < 1.0)) return GSX_ERR_ARG;
-  if (cfg->n_s < 1) return GSX_ERR_ARG;
-  if (cfg->dt_min > cfg->dt_max) return GSX_ERR_ARG;
-  if (cfg->mode != 0 && cfg->mode != 1) return GSX_ERR_ARG;
-  if (!(cfg->dt > 0.0)) return GSX_ERR_ARG;
-  return GSX_OK;
 }
 
 __global__ void k_ffma(int64_t iters, float* sink) {
@@ -300,6 +174,17 @@ __global__ void k_ffma(int64_t iters, float* sink) {
 
 }  // namespace
 
+int gsx_validate_cfg(const gsx_render_cfg* cfg) {
+  // RenderConfig.__post_init__ (renderer.py:41-49)
+  if (!cfg) return GSX_ERR_ARG;
+  if (!(cfg->t_eps > 0.0 && cfg->t_eps < 1.0)) return GSX_ERR_ARG;
+  if (cfg->n_s < 1) return GSX_ERR_ARG;
+  if (cfg->dt_min > cfg->dt_max) return GSX_ERR_ARG;
+  if (cfg->mode != 0 && cfg->mode != 1) return GSX_ERR_ARG;
+  if (!(cfg->dt > 0.0)) return GSX_ERR_ARG;
+  return GSX_OK;
+}
+
 extern "C" int gsx_calibrate_fp32(int64_t iters, float* sink, double* flops, void* stream) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -310,12 +195,23 @@ extern "C" int gsx_calibrate_fp32(int64_t iters, float* sink, double* flops, voi
   return gsx_check_launch();
 }
 
+#ifdef GSX_PHASE_PROF
+extern "C" int gsx_phase_times(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, gsx::g_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(gsx::g_phase, z, sizeof z);
+  }
+  return gsx_check_launch();
+}
+#endif
+
 extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena, int64_t n,
                                   const gsx_camera* cam, const gsx_render_cfg* cfg,
                                   int64_t tile_begin, int64_t tile_stride, float* rgb,
                                   float* depth, float* trans, gsx_stats* stats,
                                   gsx_dev_status* dev_status, void* stream) {
-  int rc = validate_cfg(cfg);
+  int rc = gsx_validate_cfg(cfg);
   if (rc) return rc;
   if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
   if (n <= 0) return GSX_ERR_EMPTY;
@@ -341,7 +237,7 @@ extern "C" int gsx_render_rays(const void* scene_arena, const void* bvh_arena, i
                                const double* rays, int64_t m, int clip,
                                const gsx_render_cfg* cfg, float* rgb, float* depth, float* trans,
                                gsx_stats* stats, gsx_dev_status* dev_status, void* stream) {
-  int rc = validate_cfg(cfg);
+  int rc = gsx_validate_cfg(cfg);
   if (rc) return rc;
   if (n <= 0) return GSX_ERR_EMPTY;
   if (m <= 0) return GSX_OK;

@@ -116,9 +116,11 @@ __device__ inline void sh_basis_f(const float* d, float* Y) {
 // unclamped radiance and lobe values (for the backward); app = 19 float4
 __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const float* Y,
                                          const float* d, float* pre, float* lobes) {
+  // SH part: floats 0..26 (coefficient-major, RGB inner)
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
   float a[76];
 #pragma unroll
-  for (int k = 0; k < 19; ++k) {
+  for (int k = 0; k < 7; ++k) {
     float4 v = __ldg(app + k);
     a[4 * k] = v.x;
     a[4 * k + 1] = v.y;
@@ -126,20 +128,32 @@ __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const f
     a[4 * k + 3] = v.w;
   }
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float s = 0.f;
+  for (int b = 0; b < 9; ++b) {
+    s0 = fmaf(Y[b], a[3 * b], s0);
+    s1 = fmaf(Y[b], a[3 * b + 1], s1);
+    s2 = fmaf(Y[b], a[3 * b + 2], s2);
+  }
+  // lobes: axes 27..47, sharpness 48..54, amplitudes 55..75
 #pragma unroll
-    for (int b = 0; b < 9; ++b) s = fmaf(Y[b], a[3 * b + ch], s);
-    pre[ch] = s;
+  for (int k = 7; k < 19; ++k) {
+    float4 v = __ldg(app + k);
+    a[4 * k] = v.x;
+    a[4 * k + 1] = v.y;
+    a[4 * k + 2] = v.z;
+    a[4 * k + 3] = v.w;
   }
 #pragma unroll
   for (int l = 0; l < 7; ++l) {
-    float cs = a[27 + 3 * l] * d[0] + a[28 + 3 * l] * d[1] + a[29 + 3 * l] * d[2];
+    float cs = fmaf(a[27 + 3 * l], d[0], fmaf(a[28 + 3 * l], d[1], a[29 + 3 * l] * d[2]));
     float e = __expf(a[48 + l] * (cs - 1.0f));
     if (lobes) lobes[l] = e;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) pre[ch] = fmaf(e, a[55 + 3 * l + ch], pre[ch]);
+    s0 = fmaf(e, a[55 + 3 * l], s0);
+    s1 = fmaf(e, a[56 + 3 * l], s1);
+    s2 = fmaf(e, a[57 + 3 * l], s2);
   }
+  pre[0] = s0;
+  pre[1] = s1;
+  pre[2] = s2;
 }
 
 __device__ inline void eval_radiance_f(const float4* __restrict__ app, const float* Y,
@@ -154,8 +168,7 @@ __device__ inline void eval_radiance_f(const float4* __restrict__ app, const flo
 // per-(ray, primitive) density setup: q(t) = A (t - tc)^2 + qmin
 // ---------------------------------------------------------------------------
 struct CandSetup {
-  float A, qmin, del0, kl2, sigma, h;
-  double tc;
+  float A, qmin, del0, kl2, sigma, h, tc, lsig;
 };
 
 __device__ inline void local_frame(const float4* geo, int64_t p, const RayCtx& r, double* y0,
@@ -170,25 +183,54 @@ __device__ inline void local_frame(const float4* geo, int64_t p, const RayCtx& r
   }
 }
 
-__device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t p, double tbase,
-                                  CandSetup& cs) {
-  double y0[3], yd[3];
-  local_frame(sv.geo, p, r, y0, yd);
-  double A = yd[0] * yd[0] + yd[1] * yd[1] + yd[2] * yd[2];
-  if (!(A > 0.0)) return false;
-  double B = y0[0] * yd[0] + y0[1] * yd[1] + y0[2] * yd[2];
-  double C = y0[0] * y0[0] + y0[1] * y0[1] + y0[2] * y0[2];
-  double tc = -B / A;
-  double qmin = fma(B, tc, C);
-  if (qmin > 1.0) return false;
-  float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1);
-  cs.A = (float)A;
-  cs.qmin = (float)qmin;
+// Sample-base point of a segment as an unevaluated float pair (x0 = hi + lo,
+// |lo| <= ulp(hi)/2), from the fp64 ray: x0 = o + tbase * d.
+struct SegBase {
+  float hi[3], lo[3];
+};
+__device__ inline SegBase seg_base(const RayCtx& r, double tbase) {
+  SegBase b;
+  for (int k = 0; k < 3; ++k) {
+    double x = fma(tbase, r.d[k], r.o[k]);
+    b.hi[k] = (float)x;
+    b.lo[k] = (float)(x - (double)b.hi[k]);
+  }
+  return b;
+}
+
+// fp32 setup relative to the segment base: v = x0 - mu is formed as
+// (hi - mu) + lo, accurate to ~ulp(|x0 - mu|) because |x0 - mu| is at most a
+// segment plus a box (~0.3 world units) for any primitive the segment can
+// see -- no catastrophic cancellation, no fp64.  Then y(j) = y0 + (j dt) yd,
+// q(j) = A (j dt - tc)^2 + qmin with qmin = |y0 + tc yd|^2.
+__device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t p,
+                                  const SegBase& b, CandSetup& cs) {
+  float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
+         g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
+  float v0 = (b.hi[0] - g0.x) + b.lo[0];
+  float v1 = (b.hi[1] - g0.y) + b.lo[1];
+  float v2 = (b.hi[2] - g0.z) + b.lo[2];
+  float y0x = fmaf(g1.x, v0, fmaf(g1.y, v1, g1.z * v2));
+  float y0y = fmaf(g2.x, v0, fmaf(g2.y, v1, g2.z * v2));
+  float y0z = fmaf(g3.x, v0, fmaf(g3.y, v1, g3.z * v2));
+  float ydx = fmaf(g1.x, r.df[0], fmaf(g1.y, r.df[1], g1.z * r.df[2]));
+  float ydy = fmaf(g2.x, r.df[0], fmaf(g2.y, r.df[1], g2.z * r.df[2]));
+  float ydz = fmaf(g3.x, r.df[0], fmaf(g3.y, r.df[1], g3.z * r.df[2]));
+  float A = fmaf(ydx, ydx, fmaf(ydy, ydy, ydz * ydz));
+  if (!(A > 0.f)) return false;
+  float B = fmaf(y0x, ydx, fmaf(y0y, ydy, y0z * ydz));
+  float tc = -B / A;
+  float ycx = fmaf(tc, ydx, y0x), ycy = fmaf(tc, ydy, y0y), ycz = fmaf(tc, ydz, y0z);
+  float qmin = fmaf(ycx, ycx, fmaf(ycy, ycy, ycz * ycz));
+  if (qmin > 1.0f) return false;
+  cs.A = A;
+  cs.qmin = qmin;
   cs.tc = tc;
-  cs.del0 = (float)(tbase - tc);
+  cs.del0 = -tc;
   cs.kl2 = g1.w;
   cs.sigma = g0.w;
-  cs.h = sqrtf(fmaxf((float)((1.0 - qmin) / A), 0.f));
+  cs.lsig = g3.w;
+  cs.h = sqrtf(fmaxf((1.0f - qmin) / A, 0.f));
   return true;
 }
 
@@ -262,11 +304,17 @@ __device__ inline float margin(const RayCtx& r, float t) {
 
 // Visit every leaf whose (outward-rounded) box slab interval overlaps
 // [t0, t1] (with a conservative margin); leaf_fn(prim) is called in traversal
-// order.  Returns false if the stack overflowed.
-template <class F>
+// order; leaf_fn returns true to stop early.  PHANTOM=false requires a true
+// ray/box intersection (tmin <= tmax) -- all a density contribution can come
+// from.  PHANTOM=true also admits the reference's "inverted" overlaps
+// (spatial.py:234,240 test a <= t1 and b >= t0 without a <= b: a box the line
+// misses whose gap [tmax, tmin] lies inside the segment still counts for
+// AABB-emptiness).  Returns false if the stack overflowed.
+template <bool PHANTOM, class F>
 __device__ inline bool traverse_segment(const BvhView& bv, const RayCtx& r, float t0, float t1,
                                         F&& leaf_fn, uint32_t& visits) {
   const float lo_t = t0 - margin(r, t0), hi_t = t1 + margin(r, t1);
+  const float gap = margin(r, t1);
   int32_t stack[GSX_STACK];
   int sp = 0;
   int32_t node = 0;
@@ -278,20 +326,20 @@ __device__ inline bool traverse_segment(const BvhView& bv, const RayCtx& r, floa
     int32_t cl = __float_as_int(a.w), cr = __float_as_int(b.w);
     float mn, mx;
     slab_f(a, b, r, mn, mx);
-    bool hl = cl != GSX_NONE && mn <= hi_t && mx >= lo_t;
+    bool hl = cl != GSX_NONE && mn <= hi_t && mx >= lo_t && (PHANTOM || mn <= mx + gap);
     slab_f(c, e, r, mn, mx);
-    bool hr = cr != GSX_NONE && mn <= hi_t && mx >= lo_t;
+    bool hr = cr != GSX_NONE && mn <= hi_t && mx >= lo_t && (PHANTOM || mn <= mx + gap);
     int32_t next = -1;
     if (hl) {
-      if (cl < 0)
-        leaf_fn((int64_t)(~cl));
-      else
+      if (cl < 0) {
+        if (leaf_fn((int64_t)(~cl))) return ok;
+      } else
         next = cl;
     }
     if (hr) {
-      if (cr < 0)
-        leaf_fn((int64_t)(~cr));
-      else if (next >= 0) {
+      if (cr < 0) {
+        if (leaf_fn((int64_t)(~cr))) return ok;
+      } else if (next >= 0) {
         if (sp < GSX_STACK)
           stack[sp++] = cr;
         else
@@ -334,7 +382,8 @@ __device__ inline bool closest_hit_r(const SceneView& sv, const BvhView& bv, con
       if (cc == GSX_NONE) continue;
       double lim = t_hi < best ? t_hi : best;
       float limf = (float)lim + margin(r, (float)lim);
-      if (!(mn[k] <= limf && mx[k] >= lo_t)) continue;
+      // a true ray/box intersection is necessary for an ellipsoid hit
+      if (!(mn[k] <= limf && mx[k] >= lo_t && mn[k] <= mx[k] + margin(r, mx[k]))) continue;
       if (cc < 0) {
         int64_t p = ~(int64_t)cc;
         double y0[3], yd[3];

@@ -1,0 +1,345 @@
+// render_warp.cuh -- warp-lockstep march machinery shared by the forward
+// (render.cu) and backward (render_bwd.cu) kernels.
+//
+// A warp = 32 spatially coherent rays (an 8x4 Z-order pixel block).  Each loop
+// iteration every active lane processes its next segment of Alg. 1
+// (renderer.py:288-358): a warp-cooperative ("packet") traversal of the 4-wide
+// BVH over the union of the 32 segments stages candidates in a shared-memory
+// list, and every lane evaluates the list against its own ray.  The backward
+// replays exactly the same code path, so its per-sample state is bit-identical
+// to the forward's.
+#pragma once
+#include "render_common.cuh"
+
+namespace gsx {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int LCAP = 256;    // warp candidate list (shared memory)
+constexpr int WSTACK = 128;  // warp traversal stack (shared memory)
+
+// Optional per-phase warp-time accounting (experiment builds only:
+// nvcc -DGSX_PHASE_PROF); compiled out of the product library.
+#ifdef GSX_PHASE_PROF
+extern __device__ unsigned long long g_phase[16];
+#define PH_BEGIN(v) \
+  __syncwarp();     \
+  long long v = clock64();
+#define PH_END(i, v) \
+  __syncwarp();      \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase[i], (unsigned long long)(clock64() - v));
+#define PH_CNT(i, val) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase[i], (unsigned long long)(val));
+#define PH_LANES(i, pred)                                                                  \
+  {                                                                                        \
+    unsigned _b = __ballot_sync(0xffffffffu, pred);                                        \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase[i], (unsigned long long)__popc(_b)); \
+  }
+#else
+#define PH_CNT(i, val)
+#define PH_LANES(i, pred)
+#define PH_BEGIN(v)
+#define PH_END(i, v)
+#endif
+
+template <bool STATS>
+struct Counters {
+  uint32_t samples = 0, segments = 0, skipped = 0, ch_calls = 0, visits = 0, aabb = 0, ell = 0,
+           pairs = 0, composited = 0;
+};
+
+struct WarpSmem {
+  int32_t stack[WSTACK];
+  int32_t list[LCAP];
+};
+
+struct WarpTrav {
+  int32_t node;
+  int sp;
+  bool done;
+  bool overflow;
+};
+
+// Warp-cooperative traversal of the 4-wide BVH: every lane tests its own
+// ray/segment against the 4 child boxes of the warp's current node,
+// __any_sync decides the (warp-uniform) descent, and leaves hit by any lane are
+// appended to the shared list.  True ray/box intersections only (see
+// traverse_segment).  Resumable: returns when done or the list is nearly full.
+__device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool want, float lo_t,
+                                     float hi_t, float gap, WarpTrav& st, WarpSmem& sm,
+                                     int& count, uint32_t& visits) {
+  const int lane = threadIdx.x & 31;
+  while (!st.done && count <= LCAP - 4) {
+    ++visits;
+    PH_CNT(8, 1)
+    const float4* nd = bv.nodes4 + 8 * (int64_t)st.node;
+    const float4 lx = __ldg(nd), ly = __ldg(nd + 1), lz = __ldg(nd + 2);
+    const float4 hx = __ldg(nd + 3), hy = __ldg(nd + 4), hz = __ldg(nd + 5);
+    const float4 cf = __ldg(nd + 6);
+    const float clo[3][4] = {{lx.x, lx.y, lx.z, lx.w}, {ly.x, ly.y, ly.z, ly.w},
+                             {lz.x, lz.y, lz.z, lz.w}};
+    const float chi[3][4] = {{hx.x, hx.y, hx.z, hx.w}, {hy.x, hy.y, hy.z, hy.w},
+                             {hz.x, hz.y, hz.z, hz.w}};
+    const int32_t ch[4] = {__float_as_int(cf.x), __float_as_int(cf.y), __float_as_int(cf.z),
+                           __float_as_int(cf.w)};
+    int32_t next = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool h = false;
+      if (want) {
+        float x0 = (clo[0][k] - r.of[0]) * r.invf[0], x1 = (chi[0][k] - r.of[0]) * r.invf[0];
+        float y0 = (clo[1][k] - r.of[1]) * r.invf[1], y1 = (chi[1][k] - r.of[1]) * r.invf[1];
+        float z0 = (clo[2][k] - r.of[2]) * r.invf[2], z1 = (chi[2][k] - r.of[2]) * r.invf[2];
+        float mn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+        float mx = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+        h = mn <= hi_t && mx >= lo_t && mn <= mx + gap;
+      }
+      const int32_t c = ch[k];
+      if (!__any_sync(FULL, h) || c == GSX_NONE) continue;
+      if (c < 0) {
+        if (lane == 0) sm.list[count] = ~c;
+        ++count;
+      } else if (next >= 0) {
+        if (st.sp < WSTACK) {
+          if (lane == 0) sm.stack[st.sp] = c;
+          ++st.sp;
+        } else {
+          st.overflow = true;
+        }
+      } else {
+        next = c;
+      }
+    }
+    __syncwarp();
+    if (next < 0) {
+      if (st.sp == 0) {
+        st.done = true;
+        break;
+      }
+      --st.sp;
+      next = sm.stack[st.sp];
+    }
+    st.node = next;
+  }
+  __syncwarp();
+}
+
+// Visit every candidate of the warp's union traversal: f(p) is called by all
+// 32 lanes in lockstep for each staged primitive p (list chunks of LCAP).
+template <class F>
+__device__ inline void for_each_candidate(const BvhView& bv, const RayCtx& r, bool want,
+                                          float lo_t, float hi_t, float gap, WarpSmem& sm,
+                                          uint32_t& visits, F&& f) {
+  WarpTrav st{0, 0, false, false};
+  int count = 0;
+  for (;;) {
+    PH_BEGIN(ph_t)
+    warp_traverse(bv, r, want, lo_t, hi_t, gap, st, sm, count, visits);
+    PH_END(1, ph_t)
+    PH_BEGIN(ph_p)
+    for (int i = 0; i < count; ++i) f((int64_t)sm.list[i]);
+    PH_END(2, ph_p)
+    __syncwarp();
+    count = 0;
+    if (st.done) break;
+  }
+}
+
+// per-lane description of the segment processed in this warp iteration
+struct Seg {
+  double t0, t1, tbase, dt, ds;
+  int m;
+};
+
+struct SegLimits {
+  float lo_t, hi_t, gap;
+};
+__device__ inline SegLimits seg_limits(const RayCtx& r, const Seg& seg) {
+  SegLimits l;
+  l.lo_t = (float)seg.t0 - margin(r, (float)seg.t0);
+  l.hi_t = (float)seg.t1 + margin(r, (float)seg.t1);
+  l.gap = margin(r, (float)seg.t1);
+  return l;
+}
+
+// Pass-1 accumulation of one candidate into the 16 per-sample sums
+// (renderer.py:218-228).  Returns whether this lane used the candidate.
+__device__ inline void accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
+                                            bool want, int mc, const SegBase& base, float dtf,
+                                            const float* Y, float (&sig)[16],
+                                            float (&W)[16][3]) {
+  CandSetup cs;
+  int jlo = 0, jhi = -1;
+  bool use = want && mc > 0 && cand_setup(sv, r, p, base, cs) &&
+             sample_range(cs, dtf, mc, jlo, jhi);
+  PH_CNT(9, 1)
+  PH_LANES(11, use)
+  PH_LANES(12, want)
+  if (!__any_sync(FULL, use)) return;
+  PH_CNT(14, 1)
+  float c[3] = {0.f, 0.f, 0.f};
+  if (use) eval_radiance_f(sv.app + 19 * p, Y, r.df, c);
+  const float nkl2 = -cs.kl2;
+  // 4-sample groups outside every lane's range are skipped warp-uniformly
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (!__any_sync(FULL, use && jlo <= 4 * g + 3 && jhi >= 4 * g)) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * g + jj;
+      float del = fmaf((float)j, dtf, cs.del0);
+      float q = fmaf(cs.A * del, del, cs.qmin);
+      if (use && q <= 1.0f) {
+        // sigma~ exp(-k q / 2) = 2^(log2 sigma~ - k log2(e) q / 2)
+        float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
+        sig[j] += dens;
+        W[j][0] = fmaf(dens, c[0], W[j][0]);
+        W[j][1] = fmaf(dens, c[1], W[j][1]);
+        W[j][2] = fmaf(dens, c[2], W[j][2]);
+      }
+    }
+  }
+}
+
+// Exact AABB-emptiness of the lane's segment (reference semantics) after the
+// true-intersection pass; STATS additionally counts every exact overlap.
+template <bool STATS>
+__device__ inline void emptiness_tail(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+                                      bool want, const Seg& seg, bool& nonempty,
+                                      Counters<STATS>& cnt) {
+  PH_BEGIN(ph_ph)
+  if (STATS) {
+    if (want) {
+      uint32_t before = cnt.aabb;
+      uint32_t v2 = 0;
+      auto count_fn = [&](int64_t p) -> bool {
+        if (exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) {
+          nonempty = true;
+          cnt.aabb++;
+          if (ellipsoid_hits_interval(sv, r, p, seg.t0, seg.t1)) cnt.ell++;
+        }
+        return false;
+      };
+      traverse_segment<true>(bv, r, (float)seg.t0, (float)seg.t1, count_fn, v2);
+      cnt.pairs += (uint32_t)seg.m * (cnt.aabb - before);
+    }
+  } else if (want && !nonempty) {
+    // no true overlap: empty unless an inverted-interval ("phantom") overlap exists
+    uint32_t v2 = 0;
+    auto probe = [&](int64_t p) -> bool {
+      if (exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
+      return nonempty;
+    };
+    traverse_segment<true>(bv, r, (float)seg.t0, (float)seg.t1, probe, v2);
+  }
+  PH_END(4, ph_ph)
+}
+
+// Alg. 1 for one lane's ray in warp lockstep (renderer.py:288-358).
+// segfn(seg, want) processes one segment for all lanes and returns the lane's
+// exact AABB-emptiness verdict (true = non-empty).
+template <bool STATS, class SegFn>
+__device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+                                  bool hit, const gsx_render_cfg& cfg, const RayAccum& acc,
+                                  Counters<STATS>& cnt, SegFn&& segfn) {
+  const int ns = (int)cfg.n_s;
+  const bool uniform = cfg.mode == 0;
+  const double t_n = r.t_n, t_f = r.t_f;
+  const double ds_u = cfg.dt * (double)ns;
+  long long k = 0, n_seg = 0;
+  double t_s = t_n;
+  bool active = hit;
+  uint32_t visits = 0;
+  PH_BEGIN(ph_all)
+  PH_BEGIN(ph_ch0)
+  if (active) {
+    if (uniform) {
+      n_seg = (long long)ceil((t_f - t_n) / ds_u);
+      if (n_seg < 1) n_seg = 1;
+    }
+    if (cfg.ess) {
+      double h;
+      if (STATS) cnt.ch_calls++;
+      if (!closest_hit_r(sv, bv, r, t_n, t_f, h, visits)) {
+        active = false;
+      } else if (uniform) {
+        long long kk = (long long)((h - t_n) / ds_u);
+        k = kk > 0 ? kk : 0;
+      } else {
+        t_s = h;
+      }
+    }
+  }
+  PH_END(0, ph_ch0)
+  while (__any_sync(FULL, active)) {
+    if (active) {
+      if (uniform)
+        active = k < n_seg && acc.transmittance() > cfg.t_eps;
+      else
+        active = t_s < t_f && acc.transmittance() > cfg.t_eps;
+    }
+    Seg seg{0, 0, 0, 0, 0, 0};
+    if (active) {
+      if (uniform) {
+        seg.t0 = t_n + (double)k * ds_u;
+        seg.t1 = seg.t0 + ds_u;
+        if (t_f < seg.t1) seg.t1 = t_f;
+        seg.dt = cfg.dt;
+        long long j0 = k * ns;
+        for (int j = 0; j < ns; ++j)
+          if (t_n + ((double)(j0 + j) + 0.5) * cfg.dt < t_f) seg.m = j + 1;
+        seg.tbase = t_n + ((double)j0 + 0.5) * cfg.dt;
+      } else {
+        seg.ds = segment_step(cfg, t_s, (double)acc.transmittance());
+        seg.dt = seg.ds / (double)ns;
+        seg.t0 = t_s;
+        seg.t1 = t_s + seg.ds;
+        if (t_f < seg.t1) seg.t1 = t_f;
+        for (int j = 0; j < ns; ++j)
+          if (t_s + ((double)j + 0.5) * seg.dt < t_f) seg.m = j + 1;
+        seg.tbase = t_s + 0.5 * seg.dt;
+      }
+    }
+    if (!__any_sync(FULL, active)) break;
+    PH_CNT(10, 1)
+    PH_LANES(13, active)
+    const bool ne = segfn(seg, active);
+    PH_BEGIN(ph_adv)
+    if (active) {
+      if (ne) {
+        if (STATS) {
+          cnt.segments++;
+          cnt.samples += seg.m;
+        }
+        if (uniform)
+          k += 1;
+        else
+          t_s = t_s + seg.ds;
+      } else {
+        if (STATS) cnt.skipped++;
+        if (cfg.ess) {
+          double h;
+          if (STATS) cnt.ch_calls++;
+          if (!closest_hit_r(sv, bv, r, seg.t1, t_f, h, visits)) {
+            active = false;
+          } else if (uniform) {
+            long long kk = (long long)((h - t_n) / ds_u);
+            k = kk > k + 1 ? kk : k + 1;
+          } else {
+            t_s = h;  // adaptive mode has no global grid: restart here
+          }
+        } else {
+          if (STATS) cnt.samples += seg.m;
+          if (uniform)
+            k += 1;
+          else
+            t_s = t_s + seg.ds;
+        }
+      }
+    }
+    PH_END(5, ph_adv)
+  }
+  PH_END(6, ph_all)
+  if (STATS) cnt.visits += visits;
+}
+
+}  // namespace gsx

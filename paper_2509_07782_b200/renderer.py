@@ -48,6 +48,29 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
     return rgb, depth, trans, st
 
 
+def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans, dL_drgb,
+                    dL_ddepth=None, dL_dtrans=None, *, grad=None, tile_begin: int = 0,
+                    tile_stride: int = 1, stream=None):
+    """Backward of `render` (no reference counterpart):
+    accumulates dL/d(records) into grad [N,87] float32 (record layout, storage
+    order; allocated zeroed unless given).  rgb/depth/trans are the forward
+    outputs of the same tiles; dL_d* are the upstream gradients (CUDA tensors)."""
+    import ctypes
+
+    cfg = cfg or RenderConfig()
+    L = _lib.lib()
+    if grad is None:
+        grad = torch.zeros((scene.n, 87), dtype=torch.float32, device=scene.device)
+    cam_c, cfg_c = camera.to_c(), cfg.to_c()
+    c = lambda t: None if t is None else t.contiguous()  # noqa: E731
+    check(L.gsx_render_backward(ptr(scene.arena), ptr(scene.bvh_arena), ptr(scene.params), scene.n,
+                                ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
+                                int(tile_stride), ptr(c(rgb)), ptr(c(depth)), ptr(c(trans)),
+                                ptr(c(dL_drgb)), ptr(c(dL_ddepth)), ptr(c(dL_dtrans)), ptr(grad),
+                                None, stream_ptr(stream)), "render_backward")
+    return grad
+
+
 def render_image(scene, camera: Camera, cfg: RenderConfig, threads: int | None = None):
     """renderer.py:396-437: returns (image (H,W,3) float64 numpy, RenderStats).
     `threads` / GSRAY_THREADS are accepted and ignored (one CUDA thread per ray)."""
