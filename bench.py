@@ -59,7 +59,51 @@ def workload(name: str):
         desc = ("C3 1M Gaussians: 70% ball r=1 + 30% background shell r=10-50 (scale ~ r), "
                 "anisotropy<=3 under r0=10 volume-ratio bound, 1920x1080, adaptive+ESS")
         return rec, 0.01, cam, dict(mode="adaptive"), desc
+    if name == "c2":
+        rec = synth_records("surface", 300_000, seed=0, anisotropy=3.0, extent=1.5,
+                            r_max_bound=10.0)
+        cam = dict(radius=4.03, focal=1111.1, width=800, height=800)
+        desc = ("C2 NeRF-synthetic-shaped: 300k Gaussians on/under a sphere of radius 1.5, "
+                "800x800, f=1111.1, white background, uniform dt=0.0025 + ESS")
+        return rec, 0.01, cam, dict(mode="uniform", background=(1.0, 1.0, 1.0)), desc
     raise ValueError(name)
+
+
+def train_step_bench(G, dev, steps: int, warmup: int):
+    """C2 training step (fwd + L1/DSSIM loss + bwd + iso loss + Adam, BVH rebuilt
+    every step) on one GPU; target = render of the scene with jittered means."""
+    import torch
+
+    from paper_2509_07782_b200.train import Trainer
+
+    rec, eps, cam_kw, cfg_kw, desc = workload("c2")
+    cam = make_camera(G, cam_kw)
+    cfg = G.RenderConfig(**cfg_kw)
+    tscene = G.Scene.from_records(rec)
+    G.reorder_by_morton(tscene)
+    target = G.render(tscene, cam, cfg)[0].clone()
+    jit = tscene.records().copy()
+    base = 0.08 * (32.0 / rec.shape[0]) ** (1.0 / 3.0)
+    jit[:, 0:3] += np.random.default_rng(1).normal(0, 0.1 * base, size=(jit.shape[0], 3))
+    scene = G.Scene.from_records(jit.astype(np.float32))
+    del tscene
+    tr = Trainer(scene, cam, cfg)
+    for _ in range(warmup):
+        tr.step(target)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = tr.step(target, want_loss=True)
+    e0.record(s)
+    for _ in range(steps):
+        tr.step(target)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    l1 = tr.step(target, want_loss=True)
+    return {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+            "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
+            "rays_per_step": cam_kw["width"] * cam_kw["height"]}
 
 
 def make_camera(G, cam):
@@ -173,6 +217,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -332,6 +377,10 @@ def main():
         "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
         "step_ms": step_ms,
     }
+    if not args.no_train and world == 1:
+        del scene
+        torch.cuda.empty_cache()
+        out["train_step"] = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3)
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

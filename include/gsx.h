@@ -204,6 +204,27 @@ int gsx_render_backward(const void* scene_arena, const void* bvh_arena, const fl
                         const float* dL_ddepth, const float* dL_dtrans, float* grad,
                         gsx_dev_status* dev_status, void* stream);
 
+/* ---- training-step kernels ---------------------------------------------------
+ * Image loss (densify.py:139-153 image_loss, :99-132 _ssim): [h,w,c] float32
+ * images, L = (1-mix) L1 + mix (1-SSIM)/2 with scipy gaussian_filter(sigma 1.5,
+ * truncate 3.5, mode 'reflect') statistics and a 5-px crop; h, w >= 11.
+ * dL_drendered (may be NULL) receives dL/d rendered; host_out (may be NULL,
+ * synchronizes the stream) receives {L, L1, SSIM}. */
+size_t gsx_image_loss_workspace_bytes(int64_t h, int64_t w, int64_t c);
+int gsx_image_loss(const float* rendered, const float* target, int64_t h, int64_t w, int64_t c,
+                   double mix, float* dL_drendered, double* host_out, void* workspace,
+                   void* stream);
+/* Isotropic loss (geometry.py:215-233): *loss_dev (device double) receives
+ * sum_i max(r_max,i - r0, 0) (divide by n for L_s); grad (may be NULL)
+ * accumulates lambda_s dL_s/ds into the scale slots [7:10] of [n,87]. */
+int gsx_iso_loss(const float* params, int64_t n, double r0, double lambda_s, float* grad,
+                 double* loss_dev, void* stream);
+/* Fused Adam over [n,87] records; lr87 = per-record-slot learning rates, lo87 =
+ * per-slot lower bounds projected after the update (device, 87 floats each). */
+int gsx_adam_step(float* params, const float* grad, float* m, float* v, int64_t n,
+                  const float* lr87, const float* lo87, double beta1, double beta2, double eps,
+                  int64_t step, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

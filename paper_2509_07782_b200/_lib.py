@@ -99,6 +99,10 @@ _SIGS = {
     "gsx_render_rays": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
     "gsx_render_backward": (INT, [P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, P, P, P]),
     "gsx_calibrate_fp32": (INT, [I64, P, P, P]),
+    "gsx_image_loss_workspace_bytes": (SZ, [I64, I64, I64]),
+    "gsx_image_loss": (INT, [P, P, I64, I64, I64, D, P, P, P, P]),
+    "gsx_iso_loss": (INT, [P, I64, D, D, P, P, P]),
+    "gsx_adam_step": (INT, [P, P, P, P, I64, P, P, D, D, D, I64, P]),
 }
 
 # Every symbol include/gsx.h declares (checked by tests/test_abi.py).

@@ -120,6 +120,22 @@ class Scene:
         """Re-derive everything after `params` was updated in place (training)."""
         self._rebuild(validate=True)
 
+    def rebuild_async(self):
+        """K1 -> K5 without any host synchronization (training hot loop): the
+        scene bounds stay on the device; validation errors are not raised
+        (the optimizer's projection keeps records valid)."""
+        L, n, s = self._L, self.n, stream_ptr()
+        check(L.gsx_prepare(ptr(self.params), n, self.sigma_eps, ptr(self.arena),
+                            ptr(self._status), None, s), "prepare")
+        check(L.gsx_scene_get(ptr(self.arena), n, 4, ptr(self.bounds_t), s), "bounds")
+        bl, bh = self.bounds_t[:3], self.bounds_t[3:]
+        check(L.gsx_morton_codes_records(ptr(self.params), n, ptr(bl), ptr(bh), ptr(self._codes),
+                                         s), "morton")
+        check(L.gsx_sort_codes(ptr(self._codes), n, ptr(self.sorted_codes), ptr(self.morton_perm),
+                               ptr(self._sort_ws), s), "sort")
+        check(L.gsx_bvh_build(ptr(self.arena), ptr(self.sorted_codes), ptr(self.morton_perm), n,
+                              ptr(self.bvh_arena), ptr(self._bvh_ws), s), "bvh")
+
     # -- reference API -------------------------------------------------------
     def __len__(self) -> int:
         return self.n

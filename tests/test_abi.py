@@ -1,0 +1,80 @@
+"""C-ABI checks on CPU (no GPU needed): libgsx.so loads, exports every symbol
+include/gsx.h declares, and the ctypes table matches the header; host-side
+config mirrors validate like the reference."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_functions():
+    src = (ROOT / "include" / "gsx.h").read_text()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gsx_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2509_07782_b200 import _lib
+
+    L = _lib.load_library()
+    funcs = header_functions()
+    assert len(funcs) >= 25
+    for f in funcs:
+        assert hasattr(L, f), f
+    assert sorted(_lib.EXPORTED) == funcs
+    assert L.gsx_abi_version() == 1
+    assert L.gsx_status_string(0) == b"ok"
+    assert L.gsx_scene_arena_bytes(1000) > 1000 * 87 * 4
+    assert L.gsx_sort_workspace_bytes(1 << 20) > 0
+
+
+def test_size_queries_and_argument_errors_without_gpu():
+    from paper_2509_07782_b200 import _lib
+
+    L = _lib.load_library()
+    # argument validation happens before any CUDA call
+    assert L.gsx_prepare(None, 0, 0.01, None, None, None, None) == _lib.GSX_ERR_EMPTY
+    assert L.gsx_prepare(ctypes.c_void_p(8), 4, -1.0, ctypes.c_void_p(8), None, None,
+                         None) == _lib.GSX_ERR_ARG
+    cfg = _lib.RenderCfg()
+    cfg.dt, cfg.n_s, cfg.t_eps, cfg.mode = 0.0025, 16, 0.0, 0
+    cam = _lib.CameraC()
+    cam.width = cam.height = 4
+    cam.focal = 1.0
+    rc = L.gsx_render_forward(None, None, 10, ctypes.byref(cam), ctypes.byref(cfg), 0, 1, None,
+                              None, None, None, None, None)
+    assert rc == _lib.GSX_ERR_ARG  # t_eps must be in (0, 1)
+    assert L.gsx_image_loss(None, None, 8, 8, 3, 0.2, None, None, None, None) == _lib.GSX_ERR_ARG
+
+
+def test_config_mirrors():
+    from paper_2509_07782_b200 import Camera, RenderConfig, segment_step
+
+    with pytest.raises(ValueError):
+        RenderConfig(mode="fancy")
+    with pytest.raises(ValueError):
+        RenderConfig(t_eps=0.0)
+    with pytest.raises(ValueError):
+        RenderConfig(dt_min=0.1, dt_max=0.01)
+    with pytest.raises(ValueError):
+        Camera(center=[0, 0, 0], quat=[1, 0, 0, 0], focal=0.0, width=4, height=4)
+    cfg = RenderConfig(mode="adaptive", beta=1024, dt_min=0.005, dt_max=0.02, n_s=16)
+    assert segment_step(cfg, 10.24, 0.125) == pytest.approx(0.32, abs=1e-12)
+    c = cfg.to_c()
+    assert c.mode == 1 and c.n_s == 16 and c.ess == 1
+
+
+def test_product_package_fails_loudly_without_gpu():
+    import torch
+
+    import paper_2509_07782_b200 as G
+    from paper_2509_07782_b200 import _lib
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_lib.GsxUnavailable):
+        G.Scene.from_records([[0.0] * 87])
