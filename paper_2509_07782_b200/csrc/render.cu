@@ -54,10 +54,11 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       W[j][0] = W[j][1] = W[j][2] = 0.f;
     }
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
-    for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, visits, [&](int64_t p) {
-      if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
-        nonempty = true;
-      accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
+    for_each_chunk(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, visits, [&](int count) {
+      accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, [&](int64_t p) {
+        if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
+          nonempty = true;
+      });
     });
     if (STATS) {
 #pragma unroll

@@ -274,6 +274,12 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
     const SegBase base = seg_base(r, tb);
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
     float gs[16], wos[16], cg[16];
+    // the candidate stream: one traversal when it fits the shared list
+    // (the common case), else chunked with a second traversal for pass 2
+    WarpTrav st{0, 0, false, false};
+    int count = 0;
+    warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+    const bool resident = st.done;
     {
       float sig[16];
       float W[16][3];
@@ -282,11 +288,17 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
         sig[j] = 0.f;
         W[j][0] = W[j][1] = W[j][2] = 0.f;
       }
-      // pass 1: the forward's exact accumulation
-      for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, visits, [&](int64_t p) {
+      // pass 1: the forward's exact accumulation (same candidate order)
+      auto exact = [&](int64_t p) {
         if (want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
-        accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
-      });
+      };
+      for (;;) {
+        accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
+        if (st.done) break;
+        __syncwarp();
+        count = 0;
+        warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+      }
       // replay the compositing and form the per-sample adjoints
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -314,12 +326,21 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
         }
       }
     }
-    if (!__any_sync(FULL, want && mc > 0)) continue;
-    // pass 2: per-primitive gradients (same deterministic candidate stream)
-    uint32_t v2 = 0;
-    for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, v2, [&](int64_t p) {
+    if (!__any_sync(FULL, want && mc > 0)) {
+      __syncwarp();
+      continue;
+    }
+    // pass 2: per-primitive gradients over the same deterministic candidate stream
+    auto pass2 = [&](int64_t p) {
       grad_candidate(sv, r, p, want, mc, base, dtf, Y, pg, gs, wos, cg, grad);
-    });
+    };
+    if (resident) {
+      for (int i = 0; i < count; ++i) pass2((int64_t)sm.list[i]);
+    } else {
+      uint32_t v2 = 0;
+      for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, v2, pass2);
+    }
+    __syncwarp();
   }
   emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt);
   return nonempty;

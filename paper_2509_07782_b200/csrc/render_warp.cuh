@@ -82,19 +82,25 @@ __device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool wa
     const int32_t ch[4] = {__float_as_int(cf.x), __float_as_int(cf.y), __float_as_int(cf.z),
                            __float_as_int(cf.w)};
     int32_t next = -1;
+    // the four child tests are independent: evaluate them together (ILP),
+    // then one ballot per child
+    bool hk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      bool h = false;
-      if (want) {
-        float x0 = (clo[0][k] - r.of[0]) * r.invf[0], x1 = (chi[0][k] - r.of[0]) * r.invf[0];
-        float y0 = (clo[1][k] - r.of[1]) * r.invf[1], y1 = (chi[1][k] - r.of[1]) * r.invf[1];
-        float z0 = (clo[2][k] - r.of[2]) * r.invf[2], z1 = (chi[2][k] - r.of[2]) * r.invf[2];
-        float mn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
-        float mx = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
-        h = mn <= hi_t && mx >= lo_t && mn <= mx + gap;
-      }
+      float x0 = (clo[0][k] - r.of[0]) * r.invf[0], x1 = (chi[0][k] - r.of[0]) * r.invf[0];
+      float y0 = (clo[1][k] - r.of[1]) * r.invf[1], y1 = (chi[1][k] - r.of[1]) * r.invf[1];
+      float z0 = (clo[2][k] - r.of[2]) * r.invf[2], z1 = (chi[2][k] - r.of[2]) * r.invf[2];
+      float mn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+      float mx = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+      hk[k] = want && mn <= hi_t && mx >= lo_t && mn <= mx + gap;
+    }
+    unsigned hits = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hits |= (__any_sync(FULL, hk[k]) ? 1u : 0u) << k;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
       const int32_t c = ch[k];
-      if (!__any_sync(FULL, h) || c == GSX_NONE) continue;
+      if (!((hits >> k) & 1u) || c == GSX_NONE) continue;
       if (c < 0) {
         if (lane == 0) sm.list[count] = ~c;
         ++count;
@@ -144,6 +150,26 @@ __device__ inline void for_each_candidate(const BvhView& bv, const RayCtx& r, bo
   }
 }
 
+// Same traversal, but f(count) is called once per staged chunk of the list.
+template <class F>
+__device__ inline void for_each_chunk(const BvhView& bv, const RayCtx& r, bool want, float lo_t,
+                                      float hi_t, float gap, WarpSmem& sm, uint32_t& visits,
+                                      F&& f) {
+  WarpTrav st{0, 0, false, false};
+  int count = 0;
+  for (;;) {
+    PH_BEGIN(ph_t)
+    warp_traverse(bv, r, want, lo_t, hi_t, gap, st, sm, count, visits);
+    PH_END(1, ph_t)
+    PH_BEGIN(ph_p)
+    f(count);
+    PH_END(2, ph_p)
+    __syncwarp();
+    count = 0;
+    if (st.done) break;
+  }
+}
+
 // per-lane description of the segment processed in this warp iteration
 struct Seg {
   double t0, t1, tbase, dt, ds;
@@ -161,19 +187,32 @@ __device__ inline SegLimits seg_limits(const RayCtx& r, const Seg& seg) {
   return l;
 }
 
-// Pass-1 accumulation of one candidate into the 16 per-sample sums
-// (renderer.py:218-228).  Returns whether this lane used the candidate.
-__device__ inline void accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
-                                            bool want, int mc, const SegBase& base, float dtf,
-                                            const float* Y, float (&sig)[16],
-                                            float (&W)[16][3]) {
+// Setup half of the pass-1 accumulation: whether this lane's samples see p.
+struct CandUse {
   CandSetup cs;
-  int jlo = 0, jhi = -1;
-  bool use = want && mc > 0 && cand_setup(sv, r, p, base, cs) &&
-             sample_range(cs, dtf, mc, jlo, jhi);
+  int jlo, jhi;
+  bool use;
+};
+__device__ inline CandUse candidate_use(const SceneView& sv, const RayCtx& r, int64_t p,
+                                        bool want, int mc, const SegBase& base, float dtf) {
+  CandUse u;
+  u.jlo = 0;
+  u.jhi = -1;
+  u.use = want && mc > 0 && cand_setup(sv, r, p, base, u.cs) &&
+          sample_range(u.cs, dtf, mc, u.jlo, u.jhi);
+  return u;
+}
+
+// Pass-1 accumulation of one candidate into the 16 per-sample sums
+// (renderer.py:218-228), given its setup.
+__device__ inline void accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
+                                       const CandUse& u, float dtf, const float* Y,
+                                       float (&sig)[16], float (&W)[16][3]) {
+  const CandSetup& cs = u.cs;
+  const bool use = u.use;
+  const int jlo = u.jlo, jhi = u.jhi;
   PH_CNT(9, 1)
   PH_LANES(11, use)
-  PH_LANES(12, want)
   if (!__any_sync(FULL, use)) return;
   PH_CNT(14, 1)
   float c[3] = {0.f, 0.f, 0.f};
@@ -197,6 +236,28 @@ __device__ inline void accumulate_candidate(const SceneView& sv, const RayCtx& r
         W[j][2] = fmaf(dens, c[2], W[j][2]);
       }
     }
+  }
+}
+
+__device__ inline void accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
+                                            bool want, int mc, const SegBase& base, float dtf,
+                                            const float* Y, float (&sig)[16],
+                                            float (&W)[16][3]) {
+  const CandUse u = candidate_use(sv, r, p, want, mc, base, dtf);
+  accumulate_used(sv, r, p, u, dtf, Y, sig, W);
+}
+
+// Pass 1 over a staged list in list order.  (Interleaving two candidates'
+// setups for ILP measured slower: the extra live state spills at 128 regs.)
+template <class Pre>
+__device__ inline void accumulate_list(const SceneView& sv, const RayCtx& r, const WarpSmem& sm,
+                                       int count, bool want, int mc, const SegBase& base,
+                                       float dtf, const float* Y, float (&sig)[16],
+                                       float (&W)[16][3], Pre&& pre) {
+  for (int i = 0; i < count; ++i) {
+    const int64_t p = sm.list[i];
+    pre(p);
+    accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
   }
 }
 
