@@ -18,11 +18,13 @@
 //   lr64   : double[n]     log_ratio        (scene.py:55)
 //   geo    : float4[n][4]  (mu, sigma~) (M row0, k*log2e/2) (M row1, k) (M row2, log2 sigma~)
 //   box32  : float[n][6]   outward-rounded fp32 AABB (LBVH leaves)
-//   app    : float4[n][19] sh 27 | unit sg axes 21 | sharpness 7 | amp 21
+//   app    : float4[n][23] radiance-streaming layout: 9 x (sh_b rgb, 0), then per
+//            lobe l: (unit axis xyz, sharpness) (amp rgb, 0)
 //   bounds : double[6]     scene AABB lo xyz, hi xyz (scene.py:66-67)
 //   part   : double[GSX_BOUNDS_BLOCKS][6] partial bounds
 // ---------------------------------------------------------------------------
 #define GSX_BOUNDS_BLOCKS 296
+#define GSX_APP_F4 23
 
 //   gaux   : float4[n][5]  backward helpers: (unit quat w,x,y,z) (1/|q_raw|, s clamped xyz)
 //            (sqrt k, scale-not-clamped mask xyz) (1/|axis_raw| lobes 0..3) (lobes 4..6, 0)
@@ -51,7 +53,7 @@ __host__ __device__ inline SceneView scene_view(void* arena, int64_t n) {
   v.lr64 = (double*)(p + off);   off += gsx_al(sizeof(double) * n);
   v.geo = (float4*)(p + off);    off += gsx_al(sizeof(float4) * 4 * n);
   v.box32 = (float*)(p + off);   off += gsx_al(sizeof(float) * 6 * n);
-  v.app = (float4*)(p + off);    off += gsx_al(sizeof(float4) * 19 * n);
+  v.app = (float4*)(p + off);    off += gsx_al(sizeof(float4) * GSX_APP_F4 * n);
   v.bounds = (double*)(p + off); off += gsx_al(sizeof(double) * 6);
   v.part = (double*)(p + off);   off += gsx_al(sizeof(double) * 6 * GSX_BOUNDS_BLOCKS);
   v.gaux = (float4*)(p + off);
@@ -65,7 +67,7 @@ inline size_t scene_arena_bytes_impl(int64_t n) {
   s += gsx_align256(sizeof(double) * n);
   s += gsx_align256(sizeof(float4) * 4 * n);
   s += gsx_align256(sizeof(float) * 6 * n);
-  s += gsx_align256(sizeof(float4) * 19 * n);
+  s += gsx_align256(sizeof(float4) * GSX_APP_F4 * n);
   s += gsx_align256(sizeof(double) * 6);
   s += gsx_align256(sizeof(double) * 6 * GSX_BOUNDS_BLOCKS);
   s += gsx_align256(sizeof(float4) * 5 * n);

@@ -101,14 +101,13 @@ __global__ void k_prepare(const float* __restrict__ params, int64_t n, double si
     b32[k] = __double2float_rd(lo[k]);
     b32[3 + k] = __double2float_ru(hi[k]);
   }
-  float a[76];
-  for (int k = 0; k < 27; ++k) a[k] = r[11 + k];
-  for (int l = 0; l < 7; ++l)
-    for (int k = 0; k < 3; ++k) a[27 + 3 * l + k] = (float)axn[l][k];
-  for (int l = 0; l < 7; ++l) a[48 + l] = r[59 + l];
-  for (int k = 0; k < 21; ++k) a[55 + k] = r[66 + k];
-  float4* ap = v.app + 19 * i;
-  for (int k = 0; k < 19; ++k) ap[k] = make_float4(a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]);
+  // radiance-streaming layout (gsx_common.cuh): SH rows, then (axis, sharpness), (amp)
+  float4* ap = v.app + GSX_APP_F4 * i;
+  for (int b = 0; b < 9; ++b) ap[b] = make_float4(r[11 + 3 * b], r[12 + 3 * b], r[13 + 3 * b], 0.f);
+  for (int l = 0; l < 7; ++l) {
+    ap[9 + 2 * l] = make_float4((float)axn[l][0], (float)axn[l][1], (float)axn[l][2], r[59 + l]);
+    ap[10 + 2 * l] = make_float4(r[66 + 3 * l], r[67 + 3 * l], r[68 + 3 * l], 0.f);
+  }
   // backward helpers (render_bwd.cu)
   float ian[7];
   for (int l = 0; l < 7; ++l) {

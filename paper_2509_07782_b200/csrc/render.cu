@@ -19,12 +19,6 @@
 #include "gsx_common.cuh"
 #include "render_warp.cuh"
 
-#ifdef GSX_PHASE_PROF
-namespace gsx {
-__device__ unsigned long long g_phase[16];
-}
-#endif
-
 namespace {
 
 using namespace gsx;
@@ -38,7 +32,6 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
                                 RayAccum& acc, Counters<STATS>& cnt, WarpSmem& sm) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
-  const SegLimits lim = seg_limits(r, seg);
   const int nchunks = (ns + 15) / 16;
   uint32_t visits = 0;
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -54,12 +47,24 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       W[j][0] = W[j][1] = W[j][2] = 0.f;
     }
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
-    for_each_chunk(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, visits, [&](int count) {
-      accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, [&](int64_t p) {
-        if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
-          nonempty = true;
-      });
-    });
+    // n_s > 16 processes the segment in 16-sample chunks, each with its own traversal
+    WarpTrav st;
+    SegLimits lim;
+    int count;
+    stage_candidates(bv, r, want, seg, sm, st, count, lim, visits);
+    auto exact = [&](int64_t p) {
+      if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
+        nonempty = true;
+    };
+    for (;;) {
+      PH_BEGIN(ph_p)
+      accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
+      PH_END(2, ph_p)
+      if (st.done) break;
+      __syncwarp();
+      count = 0;
+      warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+    }
     if (STATS) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
@@ -106,18 +111,29 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
   });
 }
 
+// CTA = FWD_THREADS rays = 256 / FWD_THREADS CTAs per 16x16 tile.  Measured on
+// C3 (ms/frame): 256x2 45.9, 128x3 48.1 (no spills), 128x4 44.9, 128x5 43.3,
+// 128x6 41.3 (85 regs, 24 warps/SM), 128x8 43.1.
+#ifndef GSX_FWD_THREADS
+#define GSX_FWD_THREADS 128
+#endif
+#ifndef GSX_FWD_MINB
+#define GSX_FWD_MINB 6
+#endif
+constexpr int FWD_THREADS = GSX_FWD_THREADS;
+constexpr int FWD_PER_TILE = 256 / FWD_THREADS;
+
 template <bool STATS>
-__global__ void __launch_bounds__(256, 2) k_render_camera(SceneView sv, BvhView bv,
-                                                          gsx_camera cam, gsx_render_cfg cfg,
-                                                          int64_t tile_begin, int64_t tile_stride,
-                                                          float* rgb, float* depth, float* trans,
-                                                          gsx_stats* stats) {
-  __shared__ WarpSmem smem[8];
+__global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
+    k_render_camera(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
+                    int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
+                    float* trans, gsx_stats* stats) {
+  __shared__ WarpSmem smem[FWD_THREADS / 32];
   int64_t W = cam.width, H = cam.height;
   int64_t tiles_x = (W + 15) / 16;
-  int64_t tile = tile_begin + (int64_t)blockIdx.x * tile_stride;
+  int64_t tile = tile_begin + (int64_t)(blockIdx.x / FWD_PER_TILE) * tile_stride;
   int mx, my;
-  morton_decode8(threadIdx.x, mx, my);
+  morton_decode8((blockIdx.x % FWD_PER_TILE) * FWD_THREADS + threadIdx.x, mx, my);
   int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
   bool valid = px < W && py < H;
   Counters<STATS> cnt;
@@ -219,18 +235,17 @@ extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena
   if (tile_stride < 1 || tile_begin < 0) return GSX_ERR_ARG;
   int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
   if (tile_begin >= tiles) return GSX_OK;
-  int64_t blocks = (tiles - tile_begin + tile_stride - 1) / tile_stride;
+  int64_t blocks = FWD_PER_TILE * ((tiles - tile_begin + tile_stride - 1) / tile_stride);
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
   cudaStream_t s = (cudaStream_t)stream;
   (void)dev_status;
   if (stats)
-    k_render_camera<true><<<(unsigned)blocks, 256, 0, s>>>(sv, bv, *cam, *cfg, tile_begin,
-                                                           tile_stride, rgb, depth, trans, stats);
+    k_render_camera<true><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
+        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, stats);
   else
-    k_render_camera<false><<<(unsigned)blocks, 256, 0, s>>>(sv, bv, *cam, *cfg, tile_begin,
-                                                            tile_stride, rgb, depth, trans,
-                                                            nullptr);
+    k_render_camera<false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
+        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr);
   return gsx_check_launch();
 }
 

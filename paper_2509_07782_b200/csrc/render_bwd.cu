@@ -177,7 +177,7 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
   float pre[3] = {0.f, 0.f, 0.f}, lob[7];
 #pragma unroll
   for (int l = 0; l < 7; ++l) lob[l] = 0.f;
-  if (use) eval_radiance_pre(sv.app + 19 * p, Y, r.df, pre, lob);
+  if (use) eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, r.df, pre, lob);
   const float c0 = fmaxf(pre[0], 0.f), c1 = fmaxf(pre[1], 0.f), c2 = fmaxf(pre[2], 0.f);
   const float gcl = pg.gC[0] * c0 + pg.gC[1] * c1 + pg.gC[2] * c2;
   const float nkl2 = -cs.kl2;
@@ -218,23 +218,15 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
     g.gp[0] = pre[0] > 0.f ? pg.gC[0] * e0 : 0.f;
     g.gp[1] = pre[1] > 0.f ? pg.gC[1] * e0 : 0.f;
     g.gp[2] = pre[2] > 0.f ? pg.gC[2] * e0 : 0.f;
-    const float4* ap = sv.app + 19 * p;
+    const float4* ap = sv.app + GSX_APP_F4 * p;
     const float4 i0 = __ldg(sv.gaux + 5 * p + 3), i1 = __ldg(sv.gaux + 5 * p + 4);
     const float inv_an[7] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z};
-    float a[76];
-#pragma unroll
-    for (int kk = 0; kk < 19; ++kk) {
-      float4 v = __ldg(ap + kk);
-      a[4 * kk] = v.x;
-      a[4 * kk + 1] = v.y;
-      a[4 * kk + 2] = v.z;
-      a[4 * kk + 3] = v.w;
-    }
 #pragma unroll
     for (int l = 0; l < 7; ++l) {
-      const float nx = a[27 + 3 * l], ny = a[28 + 3 * l], nz = a[29 + 3 * l];
-      const float lam = a[48 + l];
-      ga[l] = a[55 + 3 * l] * g.gp[0] + a[56 + 3 * l] * g.gp[1] + a[57 + 3 * l] * g.gp[2];
+      const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
+      const float nx = ax.x, ny = ax.y, nz = ax.z;
+      const float lam = ax.w;
+      ga[l] = am.x * g.gp[0] + am.y * g.gp[1] + am.z * g.gp[2];
       const float cs2 = fmaf(nx, r.df[0], fmaf(ny, r.df[1], nz * r.df[2]));
       gsh[l] = lob[l] * (cs2 - 1.f) * ga[l];
       const float f = lob[l] * lam * ga[l];
@@ -264,7 +256,6 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
                                  WarpSmem& sm, float* __restrict__ grad) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
-  const SegLimits lim = seg_limits(r, seg);
   const int nchunks = (ns + 15) / 16;
   uint32_t visits = 0;
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -274,11 +265,13 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
     const SegBase base = seg_base(r, tb);
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
     float gs[16], wos[16], cg[16];
-    // the candidate stream: one traversal when it fits the shared list
-    // (the common case), else chunked with a second traversal for pass 2
-    WarpTrav st{0, 0, false, false};
-    int count = 0;
-    warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+    // the candidate stream, staged exactly as in the forward (render.cu):
+    // resident when it fits the shared list (the common case), else chunked
+    // with a second traversal for pass 2
+    WarpTrav st;
+    SegLimits lim;
+    int count;
+    stage_candidates(bv, r, want, seg, sm, st, count, lim, visits);
     const bool resident = st.done;
     {
       float sig[16];
@@ -346,18 +339,28 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
   return nonempty;
 }
 
-__global__ void __launch_bounds__(256, 1) k_render_backward(
+// CTA = BWD_THREADS rays = 256 / BWD_THREADS CTAs per 16x16 tile
+#ifndef GSX_BWD_THREADS
+#define GSX_BWD_THREADS 256
+#endif
+#ifndef GSX_BWD_MINB
+#define GSX_BWD_MINB 1
+#endif
+constexpr int BWD_THREADS = GSX_BWD_THREADS;
+constexpr int BWD_PER_TILE = 256 / BWD_THREADS;
+
+__global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB) k_render_backward(
     SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
     int64_t tile_stride, const float* __restrict__ rgb, const float* __restrict__ depth,
     const float* __restrict__ trans, const float* __restrict__ dL_drgb,
     const float* __restrict__ dL_ddepth, const float* __restrict__ dL_dtrans,
     float* __restrict__ grad) {
-  __shared__ WarpSmem smem[8];
+  __shared__ WarpSmem smem[BWD_THREADS / 32];
   int64_t W = cam.width, H = cam.height;
   int64_t tiles_x = (W + 15) / 16;
-  int64_t tile = tile_begin + (int64_t)blockIdx.x * tile_stride;
+  int64_t tile = tile_begin + (int64_t)(blockIdx.x / BWD_PER_TILE) * tile_stride;
   int mx, my;
-  morton_decode8(threadIdx.x, mx, my);
+  morton_decode8((blockIdx.x % BWD_PER_TILE) * BWD_THREADS + threadIdx.x, mx, my);
   int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
   bool valid = px < W && py < H;
   RayCtx r;
@@ -410,10 +413,10 @@ extern "C" int gsx_render_backward(const void* scene_arena, const void* bvh_aren
   if (tile_stride < 1 || tile_begin < 0) return GSX_ERR_ARG;
   int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
   if (tile_begin >= tiles) return GSX_OK;
-  int64_t blocks = (tiles - tile_begin + tile_stride - 1) / tile_stride;
+  int64_t blocks = BWD_PER_TILE * ((tiles - tile_begin + tile_stride - 1) / tile_stride);
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
-  k_render_backward<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+  k_render_backward<<<(unsigned)blocks, BWD_THREADS, 0, (cudaStream_t)stream>>>(
       sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, dL_drgb, dL_ddepth,
       dL_dtrans, grad);
   return gsx_check_launch();

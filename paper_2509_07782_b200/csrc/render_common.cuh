@@ -113,43 +113,28 @@ __device__ inline void sh_basis_f(const float* d, float* Y) {
   Y[8] = C2C * (x * x - y * y);
 }
 
-// unclamped radiance and lobe values (for the backward); app = 19 float4
+// unclamped radiance and lobe values (lobes may be NULL); app = GSX_APP_F4
+// float4 in the streaming layout, consumed one float4 at a time so the
+// coefficients never need 76 live registers.
 __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const float* Y,
                                          const float* d, float* pre, float* lobes) {
-  // SH part: floats 0..26 (coefficient-major, RGB inner)
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-  float a[76];
-#pragma unroll
-  for (int k = 0; k < 7; ++k) {
-    float4 v = __ldg(app + k);
-    a[4 * k] = v.x;
-    a[4 * k + 1] = v.y;
-    a[4 * k + 2] = v.z;
-    a[4 * k + 3] = v.w;
-  }
 #pragma unroll
   for (int b = 0; b < 9; ++b) {
-    s0 = fmaf(Y[b], a[3 * b], s0);
-    s1 = fmaf(Y[b], a[3 * b + 1], s1);
-    s2 = fmaf(Y[b], a[3 * b + 2], s2);
-  }
-  // lobes: axes 27..47, sharpness 48..54, amplitudes 55..75
-#pragma unroll
-  for (int k = 7; k < 19; ++k) {
-    float4 v = __ldg(app + k);
-    a[4 * k] = v.x;
-    a[4 * k + 1] = v.y;
-    a[4 * k + 2] = v.z;
-    a[4 * k + 3] = v.w;
+    const float4 v = __ldg(app + b);
+    s0 = fmaf(Y[b], v.x, s0);
+    s1 = fmaf(Y[b], v.y, s1);
+    s2 = fmaf(Y[b], v.z, s2);
   }
 #pragma unroll
   for (int l = 0; l < 7; ++l) {
-    float cs = fmaf(a[27 + 3 * l], d[0], fmaf(a[28 + 3 * l], d[1], a[29 + 3 * l] * d[2]));
-    float e = __expf(a[48 + l] * (cs - 1.0f));
+    const float4 ax = __ldg(app + 9 + 2 * l), am = __ldg(app + 10 + 2 * l);
+    float cs = fmaf(ax.x, d[0], fmaf(ax.y, d[1], ax.z * d[2]));
+    float e = __expf(ax.w * (cs - 1.0f));
     if (lobes) lobes[l] = e;
-    s0 = fmaf(e, a[55 + 3 * l], s0);
-    s1 = fmaf(e, a[56 + 3 * l], s1);
-    s2 = fmaf(e, a[57 + 3 * l], s2);
+    s0 = fmaf(e, am.x, s0);
+    s1 = fmaf(e, am.y, s1);
+    s2 = fmaf(e, am.z, s2);
   }
   pre[0] = s0;
   pre[1] = s1;

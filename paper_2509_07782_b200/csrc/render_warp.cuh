@@ -20,7 +20,8 @@ constexpr int WSTACK = 128;  // warp traversal stack (shared memory)
 // Optional per-phase warp-time accounting (experiment builds only:
 // nvcc -DGSX_PHASE_PROF); compiled out of the product library.
 #ifdef GSX_PHASE_PROF
-extern __device__ unsigned long long g_phase[16];
+// one copy per translation unit (no -rdc); gsx_phase_times reads render.cu's
+static __device__ unsigned long long g_phase[16];
 #define PH_BEGIN(v) \
   __syncwarp();     \
   long long v = clock64();
@@ -179,12 +180,30 @@ struct Seg {
 struct SegLimits {
   float lo_t, hi_t, gap;
 };
-__device__ inline SegLimits seg_limits(const RayCtx& r, const Seg& seg) {
+__device__ inline SegLimits seg_limits(const RayCtx& r, const struct Seg& seg) {
   SegLimits l;
   l.lo_t = (float)seg.t0 - margin(r, (float)seg.t0);
   l.hi_t = (float)seg.t1 + margin(r, (float)seg.t1);
   l.gap = margin(r, (float)seg.t1);
   return l;
+}
+
+// Stage the candidates of this iteration's segments: traverse [t0, t1] (with
+// margins).  On return `count` entries are in sm.list; st.done == false means
+// the list is only the first chunk of a longer stream (the caller continues
+// with warp_traverse and the bounds in lim).
+// (A look-ahead window reused across iterations was measured slower: only 29%
+// of iterations could reuse it -- lanes ESS-jump or outgrow it -- while every
+// list grew by ~70%.)
+__device__ inline void stage_candidates(const BvhView& bv, const RayCtx& r, bool want,
+                                        const Seg& seg, WarpSmem& sm, WarpTrav& st, int& count,
+                                        SegLimits& lim, uint32_t& visits) {
+  lim = seg_limits(r, seg);
+  st = WarpTrav{0, 0, false, false};
+  count = 0;
+  PH_BEGIN(ph_t)
+  warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+  PH_END(1, ph_t)
 }
 
 // Setup half of the pass-1 accumulation: whether this lane's samples see p.
@@ -216,7 +235,7 @@ __device__ inline void accumulate_used(const SceneView& sv, const RayCtx& r, int
   if (!__any_sync(FULL, use)) return;
   PH_CNT(14, 1)
   float c[3] = {0.f, 0.f, 0.f};
-  if (use) eval_radiance_f(sv.app + 19 * p, Y, r.df, c);
+  if (use) eval_radiance_f(sv.app + GSX_APP_F4 * p, Y, r.df, c);
   const float nkl2 = -cs.kl2;
   // 4-sample groups outside every lane's range are skipped warp-uniformly
 #pragma unroll

@@ -42,7 +42,7 @@ tot = buf[6] or 1
 out = {n: {"warp_cycles": int(buf[i]), "share_of_march": buf[i] / tot} for i, n in enumerate(names[:7])}
 warps = (cam.width * cam.height + 31) // 32
 counts = {"warp_node_steps": buf[8], "warp_list_entries": buf[9], "warp_iterations": buf[10],
-          "lane_candidate_uses": buf[11], "lane_candidate_tests": buf[12],
+          "lane_candidate_uses": buf[11], "lane_candidate_tests": buf[12], "reuses": buf[15],
           "active_lane_iterations": buf[13],
           "per_warp": {"node_steps": buf[8] / warps, "list_entries": buf[9] / warps,
                        "iterations": buf[10] / warps},
