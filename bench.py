@@ -136,6 +136,17 @@ class ClockSampler:
         for line in self._p.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    _lo = None
+    _hi = None
+
+    def mark(self):
+        """Start of the timed region (samples before it are warm-up)."""
+        self._lo = len(self.rows)
+
+    def mark_end(self):
+        time.sleep(0.25)  # let the sampler catch the tail of the timed region
+        self._hi = len(self.rows)
+
     def __exit__(self, *a):
         if self._p:
             self._p.terminate()
@@ -145,19 +156,23 @@ class ClockSampler:
                 self._p.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        if self._lo is not None:
+            win = rows[max(self._lo - 1, 0):(self._hi or len(rows)) + 1]
+            rows = win if win else rows
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for k, nm in enumerate(names):
                 if len(r) > 5 + k and r[5 + k].lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(rows), "window": "timed region (+-1 sample, 100 ms period)"}
 
 
 # ----------------------------------------------------------------------------- CPU leg
@@ -184,16 +199,19 @@ def cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s: float = 15.0, steps: int = 
     osc.reorder_by_morton()
     build_s = time.time() - t0
     cfg = O.OCfg.make(**cfg_kw)
-    # calibrate the sample size on a sparse probe
-    stride = 256
-    probe = cpu_rays(cam_kw, stride)
-    t0 = time.time()
-    osc.march_rays(probe, cfg, clip=True, threads=threads)
-    dt = max(time.time() - t0, 1e-3)
+    # calibrate the sample size on sparse probes (large enough to amortize
+    # the thread start-up), then pick the stride that fills target_s
+    total = cam_kw["width"] * cam_kw["height"]
+    for stride in (128, 64, 32):
+        probe = cpu_rays(cam_kw, stride, 7)
+        t0 = time.time()
+        osc.march_rays(probe, cfg, clip=True, threads=threads)
+        dt = max(time.time() - t0, 1e-3)
+        if dt > 0.5:
+            break
     per_ray = dt / len(probe)
     want = target_s / max(steps, 1) / per_ray
-    total = cam_kw["width"] * cam_kw["height"]
-    stride = int(max(2, min(256, math.floor(math.sqrt(total / max(want, 1.0))))))
+    stride = int(max(1, min(256, math.floor(math.sqrt(total / max(want, 1.0))))))
     times, nrays = [], 0
     for k in range(steps):
         rays = cpu_rays(cam_kw, stride, offset0 + k)
@@ -313,25 +331,36 @@ def main():
     depth = torch.zeros((H, W), device=dev)
     trans = torch.zeros((H, W), device=dev)
     tb, ts = (rank, world) if world > 1 else (0, 1)
+    from paper_2509_07782_b200.train import assemble_tiles
 
     def step():
+        # N > 1: every rank renders its interleaved tiles; the frame is then
+        # assembled on every rank (one NCCL all-reduce of disjoint tiles)
+        if world > 1:
+            rgb.zero_()
+            depth.zero_()
+            trans.zero_()
         G.render(scene, cam, cfg, tile_begin=tb, tile_stride=ts, rgb=rgb, depth=depth,
                  trans=trans)
+        if world > 1:
+            assemble_tiles([rgb, depth, trans])
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk.mark()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         for k in range(args.steps):
             flush.zero_()
             starts[k].record(s)
             step()
             ends[k].record(s)
         torch.cuda.synchronize()
+        clk.mark_end()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     tot_ms = sum(step_ms)
     if world > 1:
@@ -362,8 +391,15 @@ def main():
     if rank != 0:
         return
     achieved = flops_frame / (ms * 1e-3) / 1e12
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu capture
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        traffic = tr.get(args.config, {}).get("k_render_camera")
+    except Exception:
+        pass
     roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak, "traffic": None,
+            "frac": achieved / fp32_peak, "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "peak_source": "measured FFMA loop (gsx_calibrate_fp32) in this run",
             "flops_per_frame": flops_frame,
             "flops_model": "33*pairs + 15*samples + 165*ellipsoid_hits + 12*node_visits (SURVEY 8(d))"}
