@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB) k_render_backward(
   Counters<false> cnt;
   const int ns = (int)cfg.n_s;
   WarpSmem& sm = smem[threadIdx.x >> 5];
-  march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, [&](const Seg& seg, bool want) {
+  march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, [&](const Seg& seg, bool want) {
     return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm, grad);
   });
 }

@@ -14,6 +14,17 @@
 namespace gsx {
 
 constexpr unsigned FULL = 0xffffffffu;
+// depth-synchronous windows (segment lengths) measured best on C3 / C2:
+// forward 1.0 (40.6 vs 41.2 ms unsynchronized), backward 0.5 (train step
+// 90 vs 125 ms).  The backward's replay then interleaves lanes differently
+// from the forward: its per-sample sums may differ from the forward's in the
+// last ulp (it uses the forward's saved C, D, T only in the adjoints).
+#ifndef GSX_SYNC_FWD
+#define GSX_SYNC_FWD 1.0f
+#endif
+#ifndef GSX_SYNC_BWD
+#define GSX_SYNC_BWD 0.5f
+#endif
 constexpr int LCAP = 256;    // warp candidate list (shared memory)
 constexpr int WSTACK = 128;  // warp traversal stack (shared memory)
 
@@ -317,10 +328,12 @@ __device__ inline void emptiness_tail(const SceneView& sv, const BvhView& bv, co
 // Alg. 1 for one lane's ray in warp lockstep (renderer.py:288-358).
 // segfn(seg, want) processes one segment for all lanes and returns the lane's
 // exact AABB-emptiness verdict (true = non-empty).
+// `sync` = depth-synchronous window in segment lengths (0 = every active lane
+// takes part every iteration).
 template <bool STATS, class SegFn>
 __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                   bool hit, const gsx_render_cfg& cfg, const RayAccum& acc,
-                                  Counters<STATS>& cnt, SegFn&& segfn) {
+                                  Counters<STATS>& cnt, float sync, SegFn&& segfn) {
   const int ns = (int)cfg.n_s;
   const bool uniform = cfg.mode == 0;
   const double t_n = r.t_n, t_f = r.t_f;
@@ -380,11 +393,25 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
       }
     }
     if (!__any_sync(FULL, active)) break;
+    // depth-synchronous scheduling: only lanes whose segment starts within
+    // GSX_SYNC segment lengths of the warp's shallowest active lane take part;
+    // lanes further ahead wait (their state is untouched, so they recompute
+    // the same segment next iteration).  Each lane still marches its own
+    // segments in its own order -- only the interleaving changes -- but the
+    // packet's union of segments stays tight.
+    bool go = active;
+    if (sync > 0.f) {
+      float t0f = active ? (float)seg.t0 : INFINITY;
+      float dmin = t0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(FULL, dmin, o));
+      go = active && t0f <= dmin + sync * (float)(seg.t1 - seg.t0);
+    }
     PH_CNT(10, 1)
-    PH_LANES(13, active)
-    const bool ne = segfn(seg, active);
+    PH_LANES(13, go)
+    const bool ne = segfn(seg, go);
     PH_BEGIN(ph_adv)
-    if (active) {
+    if (go) {
       if (ne) {
         if (STATS) {
           cnt.segments++;
