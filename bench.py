@@ -101,9 +101,36 @@ def train_step_bench(G, dev, steps: int, warmup: int):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     l1 = tr.step(target, want_loss=True)
-    return {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
-            "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
-            "rays_per_step": cam_kw["width"] * cam_kw["height"]}
+    # phase breakdown of one step (device events between the stages)
+    from paper_2509_07782_b200.renderer import render, render_backward
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev[0].record(s)
+    scene.rebuild_async()
+    ev[1].record(s)
+    render(scene, cam, cfg, rgb=tr.rgb, depth=tr.depth, trans=tr.trans, log=tr.log)
+    ev[2].record(s)
+    tr.loss(tr.rgb, target, tr.loss_cfg.mix, grad=tr.dI, want_value=False)
+    ev[3].record(s)
+    tr.grad.zero_()
+    render_backward(scene, cam, cfg, tr.rgb, tr.depth, tr.trans, tr.dI, grad=tr.grad, log=tr.log)
+    ev[4].record(s)
+    # for comparison: the replay backward (no march log)
+    tr.grad.zero_()
+    render_backward(scene, cam, cfg, tr.rgb, tr.depth, tr.trans, tr.dI, grad=tr.grad)
+    ev[5].record(s)
+    torch.cuda.synchronize()
+    phases = {"rebuild_ms": ev[0].elapsed_time(ev[1]), "forward_ms": ev[1].elapsed_time(ev[2]),
+              "loss_ms": ev[2].elapsed_time(ev[3]), "backward_ms": ev[3].elapsed_time(ev[4]),
+              "replay_backward_ms": ev[4].elapsed_time(ev[5])}
+    out = {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
+           "rays_per_step": cam_kw["width"] * cam_kw["height"], "phases": phases}
+    if tr.log is not None:
+        used, ovf = tr.log.usage()
+        out["march_log"] = {"used_bytes": used, "capacity_bytes": tr.log.capacity,
+                            "overflow": ovf}
+    return out
 
 
 def make_camera(G, cam):

@@ -204,6 +204,30 @@ int gsx_render_backward(const void* scene_arena, const void* bvh_arena, const fl
                         const float* dL_ddepth, const float* dL_dtrans, float* grad,
                         gsx_dev_status* dev_status, void* stream);
 
+/* ---- march log (training; no reference counterpart) --------------------------
+ * A training forward can record, per warp, the candidate lists and per-sample
+ * sums it computes into a device arena (`log`, log_bytes); the logged backward
+ * then skips the replay traversal and density pass.  Warps whose records do
+ * not fit are flagged and replayed by gsx_render_backward's kernel inside
+ * gsx_render_backward_logged, so any capacity >= gsx_march_log_min_bytes is
+ * correct; gsx_march_log_usage (synchronizes `stream`) reports the bytes the
+ * last forward needed and whether it overflowed.  The backward must use the
+ * same camera, cfg, tiles and scene as the logged forward. */
+int64_t gsx_march_log_min_bytes(const gsx_camera* cam, int64_t tile_begin, int64_t tile_stride);
+int gsx_render_forward_logged(const void* scene_arena, const void* bvh_arena, int64_t n,
+                              const gsx_camera* cam, const gsx_render_cfg* cfg,
+                              int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
+                              float* trans, void* log, int64_t log_bytes,
+                              gsx_dev_status* dev_status, void* stream);
+int gsx_render_backward_logged(const void* scene_arena, const void* bvh_arena,
+                               const float* params, int64_t n, const gsx_camera* cam,
+                               const gsx_render_cfg* cfg, int64_t tile_begin, int64_t tile_stride,
+                               const float* rgb, const float* depth, const float* trans,
+                               const float* dL_drgb, const float* dL_ddepth,
+                               const float* dL_dtrans, const void* log, float* grad,
+                               gsx_dev_status* dev_status, void* stream);
+int gsx_march_log_usage(const void* log, int64_t* used_bytes, int* overflow, void* stream);
+
 /* ---- training-step kernels ---------------------------------------------------
  * Image loss (densify.py:139-153 image_loss, :99-132 _ssim): [h,w,c] float32
  * images, L = (1-mix) L1 + mix (1-SSIM)/2 with scipy gaussian_filter(sigma 1.5,

@@ -8,8 +8,8 @@ kernels (libgsx.so, C ABI in include/gsx.h).  There is no CPU fallback.
 from .config import Camera, Ray, RenderConfig, RenderStats, quat_to_rotation, segment_step
 from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptyScene, GsrayError,
                      ParseError, ValidationError)
-from .renderer import (clip_ray_to_scene, march_ray, march_rays, psnr, render, render_backward,
-                       render_full, render_image)
+from .renderer import (MarchLog, clip_ray_to_scene, march_ray, march_rays, psnr, render,
+                       render_backward, render_full, render_image)
 from .scene import Scene, gen_test_scene, load_scene, reorder_by_morton, save_scene
 from .scenes import orbit_poses, look_at
 
@@ -27,7 +27,7 @@ def look_at_camera(center, target, focal, width, height, up=(0.0, 1.0, 0.0), **k
 
 
 __all__ = [
-    "BufferOverflow", "Camera", "DegenerateCenter", "EmptyIsosurface", "EmptyScene",
+    "BufferOverflow", "Camera", "DegenerateCenter", "MarchLog", "EmptyIsosurface", "EmptyScene",
     "GsrayError", "ParseError", "Ray", "RenderConfig", "RenderStats", "Scene",
     "ValidationError", "clip_ray_to_scene", "gen_test_scene", "load_scene", "look_at_camera",
     "march_ray", "march_rays", "orbit_cameras", "psnr", "quat_to_rotation", "render",

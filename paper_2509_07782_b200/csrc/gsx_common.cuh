@@ -26,8 +26,9 @@
 #define GSX_BOUNDS_BLOCKS 296
 #define GSX_APP_F4 23
 
-//   gaux   : float4[n][5]  backward helpers: (unit quat w,x,y,z) (1/|q_raw|, s clamped xyz)
-//            (sqrt k, scale-not-clamped mask xyz) (1/|axis_raw| lobes 0..3) (lobes 4..6, 0)
+//   gaux   : float4[n][5]  backward helpers: (unit quat w,x,y,z) (1/|q_raw|, 1/s clamped xyz)
+//            (sqrt k, scale-not-clamped mask xyz) (1/|axis_raw| lobes 0..3)
+//            (1/|axis_raw| lobes 4..6, 1/sigma~)
 struct SceneView {
   double* aabb64;
   double* inv64;

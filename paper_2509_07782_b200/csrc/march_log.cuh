@@ -1,0 +1,169 @@
+// march_log.cuh -- per-warp record of a training forward, consumed by the
+// backward (no reference counterpart: the reference backward is autograd /
+// finite differences).
+//
+// A training forward already computes everything the backward's replay pass
+// would recompute: the warp's candidate stream per iteration and, per lane and
+// sample, sigma_j and the colour sums W_j.  With 180 GB of HBM the cheapest
+// backward keeps them: the logged forward appends one record per warp
+// iteration (chunk) to a bump-allocated arena, the logged backward walks its
+// warp's chain, replays only the compositing from the saved sums, and runs
+// pass 2 over the saved lists -- no traversal, no density pass, no ESS.
+//
+// Arena (all offsets in bytes from the arena base, 128-byte aligned):
+//   [LogHeader, 128 B][int64 first[nw]][uint32 complete[nw]] [records ...]
+// Record = 128-byte LogRec header + body:
+//   kind 0 (full):  double tb[32], double dt[32], int32 mc[32],
+//                   float smp[mmax][4][32] (sigma, W0, W1, W2 per sample/lane),
+//                   int32 list[count]
+//   kind 1 (list):  int32 list[count]   (a leading chunk of a candidate stream
+//                   longer than the shared list; the kind-0 record that
+//                   follows holds the rest and the sample sums)
+// A warp whose records did not fit (bump pointer past capacity) is marked
+// complete = 0 and the backward recomputes it with the replay kernel.
+#pragma once
+#include "gsx_common.cuh"
+
+namespace gsx {
+
+struct LogHeader {
+  unsigned long long head;  // bump pointer (bytes)
+  unsigned long long cap;   // arena bytes
+  unsigned int overflow;
+  unsigned int nwarps;
+  unsigned int pad[26];
+};
+static_assert(sizeof(LogHeader) == 128, "LogHeader is one 128-byte line");
+
+struct LogRec {
+  long long next;  // offset of the warp's next record, -1 = last
+  int count;       // list entries in this record
+  int kind;        // 0 full, 1 list chunk
+  int mmax;        // samples stored per lane (warp max of mc), kind 0
+  int pad[27];
+};
+static_assert(sizeof(LogRec) == 128, "LogRec is one 128-byte line");
+
+constexpr long long LOG_LANE_BYTES = 32 * 8 + 32 * 8 + 32 * 4;  // tb, dt, mc
+
+__host__ __device__ inline long long log_round128(long long x) { return (x + 127) & ~127LL; }
+__host__ __device__ inline long long log_table_bytes(long long nw) {
+  return log_round128(128 + 8 * nw) + log_round128(4 * nw);
+}
+__host__ __device__ inline long long* log_first(void* base) {
+  return (long long*)((char*)base + 128);
+}
+__host__ __device__ inline unsigned* log_complete(void* base, long long nw) {
+  return (unsigned*)((char*)base + log_round128(128 + 8 * nw));
+}
+
+// warp index within a launch over a tile subset: 8 warps per 16x16 tile
+__device__ inline long long tile_warp_id(int per_tile, int threads) {
+  return (long long)(blockIdx.x / per_tile) * 8 +
+         (((blockIdx.x % per_tile) * threads + threadIdx.x) >> 5);
+}
+
+// Warp-uniform writer state of one warp of the logged forward.
+struct LogWriter {
+  char* base;
+  long long first, prev;
+  long long wid;
+  bool on;
+};
+
+__device__ inline LogWriter log_writer(void* base, long long wid) {
+  LogWriter w;
+  w.base = (char*)base;
+  w.first = -1;
+  w.prev = -1;
+  w.wid = wid;
+  w.on = base != nullptr;
+  return w;
+}
+
+// Allocate `bytes` for this warp and link it after the warp's previous record.
+// Warp-uniform; returns the offset, or -1 (and turns the writer off) on overflow.
+__device__ inline long long log_alloc(LogWriter& w, long long bytes) {
+  const int lane = threadIdx.x & 31;
+  LogHeader* h = (LogHeader*)w.base;
+  long long off = 0;
+  if (lane == 0) {
+    off = (long long)atomicAdd(&h->head, (unsigned long long)bytes);
+    if (off + bytes > (long long)h->cap) {
+      atomicExch(&h->overflow, 1u);
+      off = -1;
+    } else if (w.prev >= 0) {
+      ((LogRec*)(w.base + w.prev))->next = off;
+    }
+  }
+  off = __shfl_sync(0xffffffffu, off, 0);
+  if (off < 0) {
+    w.on = false;
+    return -1;
+  }
+  if (w.first < 0) w.first = off;
+  w.prev = off;
+  return off;
+}
+
+__device__ inline void log_header(const LogWriter& w, long long off, int count, int kind,
+                                  int mmax) {
+  if ((threadIdx.x & 31) == 0) {
+    LogRec* r = (LogRec*)(w.base + off);
+    r->next = -1;
+    r->count = count;
+    r->kind = kind;
+    r->mmax = mmax;
+  }
+}
+
+__device__ inline void log_list(int32_t* dst, const int32_t* list, int count) {
+  for (int i = threadIdx.x & 31; i < count; i += 32) dst[i] = list[i];
+}
+
+// kind 1: a full shared-list chunk of a long candidate stream
+__device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int count) {
+  if (!w.on) return;
+  const long long off = log_alloc(w, 128 + log_round128(4LL * count));
+  if (off < 0) return;
+  log_header(w, off, count, 1, 0);
+  log_list((int32_t*)(w.base + off + 128), list, count);
+}
+
+// kind 0: the lane block, the per-sample sums and the last list chunk
+__device__ inline void log_full(LogWriter& w, const int32_t* list, int count, double tb,
+                                double dt, int mc, const float (&sig)[16],
+                                const float (&W)[16][3]) {
+  if (!w.on) return;
+  const int lane = threadIdx.x & 31;
+  const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
+  const long long off =
+      log_alloc(w, 128 + LOG_LANE_BYTES + 512LL * mmax + log_round128(4LL * count));
+  if (off < 0) return;
+  log_header(w, off, count, 0, mmax);
+  char* body = w.base + off + 128;
+  ((double*)body)[lane] = tb;
+  ((double*)body)[32 + lane] = dt;
+  ((int*)(body + 512))[lane] = mc;
+  float* smp = (float*)(body + LOG_LANE_BYTES);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < mmax) {
+      const bool in = j < mc;
+      smp[(4 * j + 0) * 32 + lane] = in ? sig[j] : 0.f;
+      smp[(4 * j + 1) * 32 + lane] = in ? W[j][0] : 0.f;
+      smp[(4 * j + 2) * 32 + lane] = in ? W[j][1] : 0.f;
+      smp[(4 * j + 3) * 32 + lane] = in ? W[j][2] : 0.f;
+    }
+  }
+  log_list((int32_t*)(body + LOG_LANE_BYTES + 512LL * mmax), list, count);
+}
+
+// end of the warp: publish its chain head and whether it is complete
+__device__ inline void log_finish(const LogWriter& w, long long nw) {
+  if (!w.base || (threadIdx.x & 31) != 0) return;
+  log_first(w.base)[w.wid] = w.on ? w.first : -1;
+  log_complete(w.base, nw)[w.wid] = w.on ? 1u : 0u;
+}
+
+}  // namespace gsx

@@ -116,11 +116,12 @@ __global__ void k_prepare(const float* __restrict__ params, int64_t n, double si
   }
   float4* ga = v.gaux + 5 * i;
   ga[0] = make_float4((float)w, (float)x, (float)y, (float)z);
-  ga[1] = make_float4((float)(1.0 / qn), (float)sc[0], (float)sc[1], (float)sc[2]);
+  ga[1] = make_float4((float)(1.0 / qn), (float)(1.0 / sc[0]), (float)(1.0 / sc[1]),
+                      (float)(1.0 / sc[2]));
   ga[2] = make_float4((float)sq, (double)r[7] > 1e-7 ? 1.f : 0.f, (double)r[8] > 1e-7 ? 1.f : 0.f,
                       (double)r[9] > 1e-7 ? 1.f : 0.f);
   ga[3] = make_float4(ian[0], ian[1], ian[2], ian[3]);
-  ga[4] = make_float4(ian[4], ian[5], ian[6], 0.f);
+  ga[4] = make_float4(ian[4], ian[5], ian[6], sigma > 0.0 ? (float)(1.0 / sigma) : 0.f);
 }
 
 // scene bounds: min/max over AABBs (exact; order independent)

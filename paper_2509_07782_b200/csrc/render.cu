@@ -16,7 +16,10 @@
 // AABB-emptiness (which drives empty-space skipping) is decided with the
 // reference's exact fp64 slab test on the candidates, so ESS jumps and
 // adaptive grid restarts happen exactly where the reference's do.
+// the forward measured faster with the cold paths inlined (C3: 40.3 vs 41.2 ms)
+#define GSX_COLD inline
 #include "gsx_common.cuh"
+#include "march_log.cuh"
 #include "render_warp.cuh"
 
 namespace {
@@ -25,11 +28,13 @@ using namespace gsx;
 
 // One warp iteration over a segment (all 32 lanes; lanes with want == false
 // only help traversing).  Accumulates and composites the lane's samples and
-// returns its exact AABB-emptiness verdict.
-template <bool STATS>
+// returns its exact AABB-emptiness verdict.  SAVE (training) also appends the
+// chunk's candidate stream and per-sample sums to the warp's march log.
+template <bool STATS, bool SAVE>
 __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                 bool want, const Seg& seg, int ns, const float* Y,
-                                RayAccum& acc, Counters<STATS>& cnt, WarpSmem& sm) {
+                                RayAccum& acc, Counters<STATS>& cnt, WarpSmem& sm,
+                                LogWriter& lw) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
   const int nchunks = (ns + 15) / 16;
@@ -52,6 +57,7 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
     SegLimits lim;
     int count;
     stage_candidates(bv, r, want, seg, sm, st, count, lim, visits);
+    const bool save = SAVE && __any_sync(FULL, want && mc > 0);
     auto exact = [&](int64_t p) {
       if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
@@ -61,10 +67,12 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
       PH_END(2, ph_p)
       if (st.done) break;
+      if (save) log_list_chunk(lw, sm.list, count);
       __syncwarp();
       count = 0;
       warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
     }
+    if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
     if (STATS) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
@@ -99,15 +107,15 @@ __device__ void flush_stats(gsx_stats* st, const Counters<STATS>& c, bool is_ray
   }
 }
 
-template <bool STATS>
+template <bool STATS, bool SAVE>
 __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayCtx& r, bool hit,
                               const gsx_render_cfg& cfg, RayAccum& acc, Counters<STATS>& cnt,
-                              WarpSmem& sm) {
+                              WarpSmem& sm, LogWriter& lw) {
   float Y[9];
   sh_basis_f(r.df, Y);
   const int ns = (int)cfg.n_s;
   march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_FWD, [&](const Seg& seg, bool want) {
-    return forward_segment<STATS>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm);
+    return forward_segment<STATS, SAVE>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm, lw);
   });
 }
 
@@ -123,11 +131,11 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
 constexpr int FWD_THREADS = GSX_FWD_THREADS;
 constexpr int FWD_PER_TILE = 256 / FWD_THREADS;
 
-template <bool STATS>
+template <bool STATS, bool SAVE>
 __global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
     k_render_camera(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
                     int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
-                    float* trans, gsx_stats* stats) {
+                    float* trans, gsx_stats* stats, void* log, long long log_nw) {
   __shared__ WarpSmem smem[FWD_THREADS / 32];
   int64_t W = cam.width, H = cam.height;
   int64_t tiles_x = (W + 15) / 16;
@@ -141,7 +149,9 @@ __global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
   bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
   RayAccum acc;
   acc.init();
-  march_forward<STATS>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5]);
+  LogWriter lw = log_writer(SAVE ? log : nullptr, tile_warp_id(FWD_PER_TILE, FWD_THREADS));
+  march_forward<STATS, SAVE>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
+  if (SAVE) log_finish(lw, log_nw);
   if (valid) {
     int64_t pix = py * W + px;
     float T = hit ? acc.transmittance() : 1.f;
@@ -166,7 +176,8 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv
   bool hit = valid && explicit_ray(rays + 8 * i, clip != 0, sv.bounds, r);
   RayAccum acc;
   acc.init();
-  march_forward<STATS>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5]);
+  LogWriter lw = log_writer(nullptr, 0);
+  march_forward<STATS, false>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
   if (valid) {
     float T = hit ? acc.transmittance() : 1.f;
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = acc.C[k] + T * (float)cfg.background[k];
@@ -241,12 +252,66 @@ extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena
   cudaStream_t s = (cudaStream_t)stream;
   (void)dev_status;
   if (stats)
-    k_render_camera<true><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
-        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, stats);
+    k_render_camera<true, false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
+        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, stats, nullptr, 0);
   else
-    k_render_camera<false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
-        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr);
+    k_render_camera<false, false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
+        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr, nullptr, 0);
   return gsx_check_launch();
+}
+
+__global__ void k_log_init(LogHeader* h, unsigned long long cap, unsigned nw, long long table) {
+  h->head = (unsigned long long)table;
+  h->cap = cap;
+  h->overflow = 0;
+  h->nwarps = nw;
+}
+
+extern "C" int64_t gsx_march_log_min_bytes(const gsx_camera* cam, int64_t tile_begin,
+                                           int64_t tile_stride) {
+  if (!cam || cam->width < 1 || cam->height < 1 || tile_stride < 1 || tile_begin < 0) return -1;
+  int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+  int64_t ntl = tile_begin >= tiles ? 0 : (tiles - tile_begin + tile_stride - 1) / tile_stride;
+  return log_table_bytes(8 * ntl);
+}
+
+extern "C" int gsx_render_forward_logged(const void* scene_arena, const void* bvh_arena,
+                                         int64_t n, const gsx_camera* cam,
+                                         const gsx_render_cfg* cfg, int64_t tile_begin,
+                                         int64_t tile_stride, float* rgb, float* depth,
+                                         float* trans, void* log, int64_t log_bytes,
+                                         gsx_dev_status* dev_status, void* stream) {
+  int rc = gsx_validate_cfg(cfg);
+  if (rc) return rc;
+  if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
+  if (n <= 0) return GSX_ERR_EMPTY;
+  if (tile_stride < 1 || tile_begin < 0 || !log) return GSX_ERR_ARG;
+  const int64_t table = gsx_march_log_min_bytes(cam, tile_begin, tile_stride);
+  if (log_bytes < table) return GSX_ERR_ARG;
+  int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+  if (tile_begin >= tiles) return GSX_OK;
+  const int64_t ntl = (tiles - tile_begin + tile_stride - 1) / tile_stride;
+  SceneView sv = scene_view((void*)scene_arena, n);
+  BvhView bv = bvh_view((void*)bvh_arena, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  (void)dev_status;
+  k_log_init<<<1, 1, 0, s>>>((LogHeader*)log, (unsigned long long)log_bytes,
+                             (unsigned)(8 * ntl), table);
+  k_render_camera<false, true><<<(unsigned)(FWD_PER_TILE * ntl), FWD_THREADS, 0, s>>>(
+      sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr, log, 8 * ntl);
+  return gsx_check_launch();
+}
+
+extern "C" int gsx_march_log_usage(const void* log, int64_t* used_bytes, int* overflow,
+                                   void* stream) {
+  if (!log) return GSX_ERR_ARG;
+  LogHeader h;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_CHECK_RET(cudaMemcpyAsync(&h, log, sizeof h, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK_RET(cudaStreamSynchronize(s));
+  if (used_bytes) *used_bytes = (int64_t)h.head;
+  if (overflow) *overflow = (int)h.overflow;
+  return GSX_OK;
 }
 
 extern "C" int gsx_render_rays(const void* scene_arena, const void* bvh_arena, int64_t n,

@@ -20,6 +20,7 @@
 // a warp-shuffle reduce-scatter (3 x 31 shuffles) and each lane issues one
 // atomic per value it owns.
 #include "gsx_common.cuh"
+#include "march_log.cuh"
 #include "render_warp.cuh"
 
 namespace {
@@ -31,59 +32,17 @@ struct PixelGrad {
   float Ctot[3], Dtot, Tend;
 };
 
-// 32 values per lane -> lane L holds the warp sum of value L.
-__device__ inline float reduce_scatter32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-  float a16[16];
-  {
-    const bool up = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float keep = up ? v[i + 16] : v[i], send = up ? v[i] : v[i + 16];
-      a16[i] = keep + __shfl_xor_sync(FULL, send, 16);
-    }
-  }
-  float a8[8];
-  {
-    const bool up = lane & 8;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float keep = up ? a16[i + 8] : a16[i], send = up ? a16[i] : a16[i + 8];
-      a8[i] = keep + __shfl_xor_sync(FULL, send, 8);
-    }
-  }
-  float a4[4];
-  {
-    const bool up = lane & 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float keep = up ? a8[i + 4] : a8[i], send = up ? a8[i] : a8[i + 4];
-      a4[i] = keep + __shfl_xor_sync(FULL, send, 4);
-    }
-  }
-  float a2[2];
-  {
-    const bool up = lane & 2;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      float keep = up ? a4[i + 2] : a4[i], send = up ? a4[i] : a4[i + 2];
-      a2[i] = keep + __shfl_xor_sync(FULL, send, 2);
-    }
-  }
-  const bool up = lane & 1;
-  float keep = up ? a2[1] : a2[0], send = up ? a2[0] : a2[1];
-  return keep + __shfl_xor_sync(FULL, send, 1);
-}
+// Gradient rows of one warp's shared reduction buffer: row = record slot
+// (0-2 mu, 3-6 q, 7-9 s, 10 sigma~, 11-37 SH, 38-58 SG axes, 59-65 SG
+// sharpness, 66-86 SG amplitudes), column = lane; padded to 33 columns so
+// both the column writes and the row sums are bank-conflict free.
+constexpr int RED_ROW = 33;
+constexpr int RED_FLOATS = GSX_NREC * RED_ROW;  // per warp
 
-// Per-(lane, primitive) gradient of the 87-float record, given the moments.
-struct CandGrad {
-  float gmu[3], gq[4], gs[3], gsig;
-  float gp[3];  // dL/d(pre-clamp radiance)
-};
-
+// Geometry rows (mu, q, s, sigma~) of one (lane, primitive) from the moments.
 __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64_t p,
                                      const SegBase& b, float m0, float m1, float m2,
-                                     CandGrad& g) {
+                                     float* __restrict__ col) {
   const float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
                g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
   const float4 a0 = __ldg(sv.gaux + 5 * p), a1 = __ldg(sv.gaux + 5 * p + 1),
@@ -104,9 +63,9 @@ __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64
   for (int a = 0; a < 3; ++a) w3[a] = fmaf(y0[a], m0, yd[a] * m1);
 #pragma unroll
   for (int a = 0; a < 3; ++a)
-    g.gmu[a] = k * fmaf(M[a], w3[0], fmaf(M[3 + a], w3[1], M[6 + a] * w3[2]));
-  // scales and rotation
-  const float s[3] = {a1.y, a1.z, a1.w};
+    col[a * RED_ROW] = k * fmaf(M[a], w3[0], fmaf(M[3 + a], w3[1], M[6 + a] * w3[2]));
+  // scales and rotation (a1.yzw = 1/s, a2.yzw = not-clamped masks)
+  const float is[3] = {a1.y, a1.z, a1.w};
   const float mask[3] = {a2.y, a2.z, a2.w};
   float u0[3], ud[3];
 #pragma unroll
@@ -117,7 +76,7 @@ __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64
 #pragma unroll
   for (int bb = 0; bb < 3; ++bb) {
     float t = fmaf(u0[bb] * u0[bb], m0, fmaf(2.f * u0[bb] * ud[bb], m1, ud[bb] * ud[bb] * m2));
-    g.gs[bb] = mask[bb] * t / s[bb];
+    col[(7 + bb) * RED_ROW] = mask[bb] * t * is[bb];
   }
   float gR[9];
 #pragma unroll
@@ -126,7 +85,7 @@ __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64
     for (int bb = 0; bb < 3; ++bb)
       gR[3 * a + bb] = -fmaf(u0[bb] * v0[a], m0,
                              fmaf(fmaf(u0[bb], r.df[a], ud[bb] * v0[a]), m1,
-                                  ud[bb] * r.df[a] * m2)) / s[bb];
+                                  ud[bb] * r.df[a] * m2)) * is[bb];
   // R(q) with q normalized (geometry.py:26-42): dR/dq, then the normalization
   const float w = a0.x, X = a0.y, Yq = a0.z, Z = a0.w;
   const float dR[4][9] = {
@@ -145,41 +104,54 @@ __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64
   const float qv[4] = {w, X, Yq, Z};
   float dot = gq[0] * w + gq[1] * X + gq[2] * Yq + gq[3] * Z;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) g.gq[c] = (gq[c] - dot * qv[c]) * a1.x;
-  g.gsig = m0 / g0.w;
+  for (int c = 0; c < 4; ++c) col[(3 + c) * RED_ROW] = (gq[c] - dot * qv[c]) * a1.x;
+  col[10 * RED_ROW] = m0 * __ldg(sv.gaux + 5 * p + 4).w;  // / sigma~
 }
 
-template <int G>
-__device__ inline float record_value(int idx, const CandGrad& g, const float* Y, const float* lob,
-                                     const float* ga, const float (*gax)[3], const float* gsh) {
-  if (idx < 3) return g.gmu[idx];
-  if (idx < 7) return g.gq[idx - 3];
-  if (idx < 10) return g.gs[idx - 7];
-  if (idx == 10) return g.gsig;
-  if (idx < 38) return Y[(idx - 11) / 3] * g.gp[(idx - 11) % 3];
-  if (idx < 59) return gax[(idx - 38) / 3][(idx - 38) % 3];
-  if (idx < 66) return gsh[idx - 59];
-  if (idx < 87) return lob[(idx - 66) / 3] * g.gp[(idx - 66) % 3];
-  return 0.f;
+// Replay one composited sample (the forward's RayAccum::add_sample) and form
+// its adjoint terms: pass 2 uses G_j = dens_j (wos_j gC.c + h_j) with
+// wos_j = w_j / sigma_j and h_j = dL/dsigma_j - wos_j gC.c_j.
+__device__ inline void sample_adjoint(RayAccum& acc, const PixelGrad& pg, float sj,
+                                      const float* Wj, float tj, float dtf, float& wos,
+                                      float& h) {
+  const float Tj = acc.T;
+  acc.add_sample(sj, Wj, tj, dtf);
+  if (sj > 0.f) {
+    const float ods = sj * dtf;
+    const float w = -expm1f(-ods) * Tj;  // the forward's w_j
+    const float s = w / sj;
+    const float cgj = (pg.gC[0] * Wj[0] + pg.gC[1] * Wj[1] + pg.gC[2] * Wj[2]) / sj;
+    const float after = pg.gC[0] * (pg.Ctot[0] - acc.C[0]) + pg.gC[1] * (pg.Ctot[1] - acc.C[1]) +
+                        pg.gC[2] * (pg.Ctot[2] - acc.C[2]);
+    const float T1 = acc.T;
+    const float gs =
+        dtf * (T1 * cgj - after + pg.gD * (T1 * tj - (pg.Dtot - acc.D)) - pg.gTe * pg.Tend);
+    wos = s;
+    h = fmaf(-s, cgj, gs);
+  }
 }
 
-// pass 2 for one staged candidate (all lanes in lockstep)
+// pass 2 for one staged candidate (all lanes in lockstep).  Every lane writes
+// its 87 values (zeros when it does not see p) as one column of the warp's
+// buffer `red` as soon as they are formed, then lane L sums rows L, L+32,
+// L+64 and issues one atomic per non-zero row: short live ranges, one copy
+// of the reduction, coalesced atomics.
 __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int64_t p, bool want,
                                       int mc, const SegBase& base, float dtf, const float* Y,
-                                      const PixelGrad& pg, const float (&gs)[16],
-                                      const float (&wos)[16], const float (&cg)[16],
+                                      const PixelGrad& pg, const float (&wos)[16],
+                                      const float (&hh)[16], float* __restrict__ red,
                                       float* __restrict__ grad) {
   CandSetup cs;
   int jlo = 0, jhi = -1;
   bool use = want && mc > 0 && cand_setup(sv, r, p, base, cs) &&
              sample_range(cs, dtf, mc, jlo, jhi);
   if (!__any_sync(FULL, use)) return;
-  float pre[3] = {0.f, 0.f, 0.f}, lob[7];
-#pragma unroll
-  for (int l = 0; l < 7; ++l) lob[l] = 0.f;
-  if (use) eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, r.df, pre, lob);
-  const float c0 = fmaxf(pre[0], 0.f), c1 = fmaxf(pre[1], 0.f), c2 = fmaxf(pre[2], 0.f);
-  const float gcl = pg.gC[0] * c0 + pg.gC[1] * c1 + pg.gC[2] * c2;
+  const int lane = threadIdx.x & 31;
+  float* col = red + lane;
+  float pre[3];
+  eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, r.df, pre, nullptr);
+  const float gcl =
+      pg.gC[0] * fmaxf(pre[0], 0.f) + pg.gC[1] * fmaxf(pre[1], 0.f) + pg.gC[2] * fmaxf(pre[2], 0.f);
   const float nkl2 = -cs.kl2;
   float m0 = 0.f, m1 = 0.f, m2 = 0.f, e0 = 0.f;
 #pragma unroll
@@ -192,7 +164,7 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
       float q = fmaf(cs.A * del, del, cs.qmin);
       if (use && q <= 1.0f) {
         float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
-        float G = fmaf(wos[j], gcl - cg[j], gs[j]) * dens;
+        float G = fmaf(wos[j], gcl, hh[j]) * dens;
         float t = (float)j * dtf;
         m0 += G;
         m1 = fmaf(G, t, m1);
@@ -201,59 +173,59 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
       }
     }
   }
-  CandGrad g;
-  float ga[7], gax[7][3], gsh[7];
+  // lanes that do not see p have zero moments: every value below is 0
+  geometry_grad(sv, r, p, base, m0, m1, m2, col);
+  float gp[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) g.gmu[i] = g.gs[i] = g.gp[i] = 0.f;
+  for (int c = 0; c < 3; ++c) gp[c] = (use && pre[c] > 0.f) ? pg.gC[c] * e0 : 0.f;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) g.gq[i] = 0.f;
-  g.gsig = 0.f;
+  for (int bsh = 0; bsh < 9; ++bsh)
 #pragma unroll
+    for (int c = 0; c < 3; ++c) col[(11 + 3 * bsh + c) * RED_ROW] = Y[bsh] * gp[c];
+  // spherical-Gaussian lobes, one at a time (rolled: keeps the 14 float4 of
+  // lobe data out of registers); the lobe value is recomputed, not kept
+  const float4* ap = sv.app + GSX_APP_F4 * p;
+  const float* inv_an = (const float*)(sv.gaux + 5 * p + 3);
+#pragma unroll 1
   for (int l = 0; l < 7; ++l) {
-    ga[l] = gsh[l] = 0.f;
-    gax[l][0] = gax[l][1] = gax[l][2] = 0.f;
+    const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
+    const float cs2 = fmaf(ax.x, r.df[0], fmaf(ax.y, r.df[1], ax.z * r.df[2]));
+    const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
+    const float ga = am.x * gp[0] + am.y * gp[1] + am.z * gp[2];
+    float* c = col + l * RED_ROW;
+    c[59 * RED_ROW] = lb * (cs2 - 1.f) * ga;
+    const float f = lb * ax.w * ga;
+    // d/d(raw axis) of the unit axis: (I - n n^T) / |a| applied to f d
+    const float dd = f * cs2, ia = __ldg(inv_an + l);
+    c[(38 + 2 * l) * RED_ROW] = fmaf(f, r.df[0], -dd * ax.x) * ia;
+    c[(39 + 2 * l) * RED_ROW] = fmaf(f, r.df[1], -dd * ax.y) * ia;
+    c[(40 + 2 * l) * RED_ROW] = fmaf(f, r.df[2], -dd * ax.z) * ia;
+    c[(66 + 2 * l) * RED_ROW] = lb * gp[0];
+    c[(67 + 2 * l) * RED_ROW] = lb * gp[1];
+    c[(68 + 2 * l) * RED_ROW] = lb * gp[2];
   }
-  if (use) {
-    geometry_grad(sv, r, p, base, m0, m1, m2, g);
-    g.gp[0] = pre[0] > 0.f ? pg.gC[0] * e0 : 0.f;
-    g.gp[1] = pre[1] > 0.f ? pg.gC[1] * e0 : 0.f;
-    g.gp[2] = pre[2] > 0.f ? pg.gC[2] * e0 : 0.f;
-    const float4* ap = sv.app + GSX_APP_F4 * p;
-    const float4 i0 = __ldg(sv.gaux + 5 * p + 3), i1 = __ldg(sv.gaux + 5 * p + 4);
-    const float inv_an[7] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z};
+  __syncwarp();
+  float* gdst = grad + (int64_t)GSX_NREC * p;
+  for (int row = lane; row < GSX_NREC; row += 32) {
+    const float* rp = red + row * RED_ROW;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-    for (int l = 0; l < 7; ++l) {
-      const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
-      const float nx = ax.x, ny = ax.y, nz = ax.z;
-      const float lam = ax.w;
-      ga[l] = am.x * g.gp[0] + am.y * g.gp[1] + am.z * g.gp[2];
-      const float cs2 = fmaf(nx, r.df[0], fmaf(ny, r.df[1], nz * r.df[2]));
-      gsh[l] = lob[l] * (cs2 - 1.f) * ga[l];
-      const float f = lob[l] * lam * ga[l];
-      const float gn[3] = {f * r.df[0], f * r.df[1], f * r.df[2]};
-      const float dd = gn[0] * nx + gn[1] * ny + gn[2] * nz;
-      gax[l][0] = (gn[0] - dd * nx) * inv_an[l];
-      gax[l][1] = (gn[1] - dd * ny) * inv_an[l];
-      gax[l][2] = (gn[2] - dd * nz) * inv_an[l];
+    for (int k = 0; k < 32; k += 4) {
+      s0 += rp[k];
+      s1 += rp[k + 1];
+      s2 += rp[k + 2];
+      s3 += rp[k + 3];
     }
+    const float sum = (s0 + s1) + (s2 + s3);
+    if (sum != 0.f) atomicAdd(gdst + row, sum);
   }
-  const int lane = threadIdx.x & 31;
-  float* gp = grad + (int64_t)GSX_NREC * p;
-#pragma unroll
-  for (int grp = 0; grp < 3; ++grp) {
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = record_value<0>(32 * grp + i, g, Y, lob, ga, gax, gsh);
-    float s = reduce_scatter32(v);
-    const int idx = 32 * grp + lane;
-    if (idx < GSX_NREC && s != 0.f) atomicAdd(gp + idx, s);
-  }
+  __syncwarp();
 }
 
 __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                  bool want, const Seg& seg, int ns, const float* Y,
                                  RayAccum& acc, const PixelGrad& pg, Counters<false>& cnt,
-                                 WarpSmem& sm, float* __restrict__ grad) {
+                                 WarpSmem& sm, float* __restrict__ red, float* __restrict__ grad) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
   const int nchunks = (ns + 15) / 16;
@@ -264,7 +236,7 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
     const double tb = seg.tbase + (double)(ch * 16) * seg.dt;
     const SegBase base = seg_base(r, tb);
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
-    float gs[16], wos[16], cg[16];
+    float wos[16], hh[16];
     // the candidate stream, staged exactly as in the forward (render.cu):
     // resident when it fits the shared list (the common case), else chunked
     // with a second traversal for pass 2
@@ -295,51 +267,93 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
       // replay the compositing and form the per-sample adjoints
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        gs[j] = wos[j] = cg[j] = 0.f;
-        if (j < mc) {
-          const float tj = (float)(tb + (double)j * seg.dt);
-          const float sj = sig[j];
-          const float Tj = acc.T;
-          acc.add_sample(sj, W[j], tj, dtf);
-          if (sj > 0.f) {
-            const float ods = sj * dtf;
-            const float w = -expm1f(-ods) * Tj;  // the forward's w_j (RayAccum::add_sample)
-            const float s = w / sj;
-            const float isg = 1.f / sj;
-            const float cgj = (pg.gC[0] * W[j][0] + pg.gC[1] * W[j][1] + pg.gC[2] * W[j][2]) * isg;
-            const float after = pg.gC[0] * (pg.Ctot[0] - acc.C[0]) +
-                                pg.gC[1] * (pg.Ctot[1] - acc.C[1]) +
-                                pg.gC[2] * (pg.Ctot[2] - acc.C[2]);
-            const float T1 = acc.T;
-            gs[j] = dtf * (T1 * cgj - after + pg.gD * (T1 * tj - (pg.Dtot - acc.D)) -
-                           pg.gTe * pg.Tend);
-            wos[j] = s;
-            cg[j] = cgj;
-          }
-        }
+        wos[j] = hh[j] = 0.f;
+        if (j < mc)
+          sample_adjoint(acc, pg, sig[j], W[j], (float)(tb + (double)j * seg.dt), dtf, wos[j],
+                         hh[j]);
       }
     }
     if (!__any_sync(FULL, want && mc > 0)) {
       __syncwarp();
       continue;
     }
-    // pass 2: per-primitive gradients over the same deterministic candidate stream
-    auto pass2 = [&](int64_t p) {
-      grad_candidate(sv, r, p, want, mc, base, dtf, Y, pg, gs, wos, cg, grad);
-    };
-    if (resident) {
-      for (int i = 0; i < count; ++i) pass2((int64_t)sm.list[i]);
-    } else {
-      uint32_t v2 = 0;
-      for_each_candidate(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, sm, v2, pass2);
-    }
+#ifdef GSX_BWD_NO_PASS2  // timing experiment only: replay without pass 2
     __syncwarp();
+    continue;
+#endif
+    // pass 2: per-primitive gradients over the same deterministic candidate
+    // stream (the resident list, or a re-traversal in chunks).  One call site
+    // of grad_candidate: the kernel is instruction-cache bound (ncu
+    // stall_no_inst), so its largest body must not be inlined twice.
+    WarpTrav st2 = st;
+    if (!resident) {
+      st2 = WarpTrav{0, 0, false, false};
+      count = 0;
+    }
+    uint32_t v2 = 0;
+    for (;;) {
+      if (!st2.done) warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st2, sm, count, v2);
+      for (int i = 0; i < count; ++i)
+        grad_candidate(sv, r, (int64_t)sm.list[i], want, mc, base, dtf, Y, pg, wos, hh, red,
+                       grad);
+      __syncwarp();
+      if (st2.done) break;
+      count = 0;
+    }
   }
   emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt);
   return nonempty;
 }
 
-// CTA = BWD_THREADS rays = 256 / BWD_THREADS CTAs per 16x16 tile
+// Per-pixel adjoint inputs from the saved frame outputs.
+struct BwdImages {
+  const float *rgb, *depth, *trans, *dL_drgb, *dL_ddepth, *dL_dtrans;
+};
+__device__ inline PixelGrad pixel_grad(const BwdImages& im, const gsx_render_cfg& cfg, bool valid,
+                                       int64_t pix) {
+  PixelGrad pg;
+  if (!valid) return PixelGrad{{0.f, 0.f, 0.f}, 0.f, 0.f, {0.f, 0.f, 0.f}, 0.f, 1.f};
+  pg.Tend = im.trans[pix];
+  pg.Dtot = im.depth[pix];
+  pg.gD = im.dL_ddepth ? im.dL_ddepth[pix] : 0.f;
+  float gTe = im.dL_dtrans ? im.dL_dtrans[pix] : 0.f;
+  for (int k = 0; k < 3; ++k) {
+    pg.gC[k] = im.dL_drgb[3 * pix + k];
+    pg.Ctot[k] = im.rgb[3 * pix + k] - pg.Tend * (float)cfg.background[k];
+    gTe = fmaf(pg.gC[k], (float)cfg.background[k], gTe);
+  }
+  pg.gTe = gTe;
+  return pg;
+}
+
+// Pixel of this thread (16x16 tiles, Z-order inside the tile) and its ray;
+// lanes without a ray get a benign direction (their values are all masked).
+__device__ inline bool tile_pixel_ray(const SceneView& sv, const gsx_camera& cam,
+                                      int64_t tile_begin, int64_t tile_stride, int per_tile,
+                                      int threads, RayCtx& r, bool& hit, int64_t& pix) {
+  const int64_t W = cam.width, H = cam.height;
+  const int64_t tiles_x = (W + 15) / 16;
+  const int64_t tile = tile_begin + (int64_t)(blockIdx.x / per_tile) * tile_stride;
+  int mx, my;
+  morton_decode8((blockIdx.x % per_tile) * threads + threadIdx.x, mx, my);
+  const int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
+  const bool valid = px < W && py < H;
+  hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
+  if (!hit) {
+    for (int k = 0; k < 3; ++k) {
+      r.o[k] = 0.0;
+      r.d[k] = k == 2 ? 1.0 : 0.0;
+      r.of[k] = 0.f;
+      r.df[k] = k == 2 ? 1.f : 0.f;
+    }
+  }
+  pix = valid ? py * W + px : 0;
+  return valid;
+}
+
+// Replay backward: CTA = BWD_THREADS rays = 256 / BWD_THREADS CTAs per tile.
+// With `skip` (a march log's complete flags) it only handles the warps the
+// log does not cover.
 #ifndef GSX_BWD_THREADS
 #define GSX_BWD_THREADS 256
 #endif
@@ -349,39 +363,19 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
 constexpr int BWD_THREADS = GSX_BWD_THREADS;
 constexpr int BWD_PER_TILE = 256 / BWD_THREADS;
 
-__global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB) k_render_backward(
-    SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
-    int64_t tile_stride, const float* __restrict__ rgb, const float* __restrict__ depth,
-    const float* __restrict__ trans, const float* __restrict__ dL_drgb,
-    const float* __restrict__ dL_ddepth, const float* __restrict__ dL_dtrans,
-    float* __restrict__ grad) {
+__global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
+    k_render_backward(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
+                      int64_t tile_begin, int64_t tile_stride, BwdImages im,
+                      const unsigned* __restrict__ skip, float* __restrict__ grad) {
   __shared__ WarpSmem smem[BWD_THREADS / 32];
-  int64_t W = cam.width, H = cam.height;
-  int64_t tiles_x = (W + 15) / 16;
-  int64_t tile = tile_begin + (int64_t)(blockIdx.x / BWD_PER_TILE) * tile_stride;
-  int mx, my;
-  morton_decode8((blockIdx.x % BWD_PER_TILE) * BWD_THREADS + threadIdx.x, mx, my);
-  int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
-  bool valid = px < W && py < H;
+  extern __shared__ float red_smem[];  // RED_FLOATS per warp
+  if (skip && skip[tile_warp_id(BWD_PER_TILE, BWD_THREADS)]) return;  // warp-uniform
   RayCtx r;
-  bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
-  PixelGrad pg;
-  if (valid) {
-    int64_t pix = py * W + px;
-    pg.Tend = trans[pix];
-    pg.Dtot = depth[pix];
-    pg.gD = dL_ddepth ? dL_ddepth[pix] : 0.f;
-    float gT = dL_dtrans ? dL_dtrans[pix] : 0.f;
-    float gTe = gT;
-    for (int k = 0; k < 3; ++k) {
-      pg.gC[k] = dL_drgb[3 * pix + k];
-      pg.Ctot[k] = rgb[3 * pix + k] - pg.Tend * (float)cfg.background[k];
-      gTe = fmaf(pg.gC[k], (float)cfg.background[k], gTe);
-    }
-    pg.gTe = gTe;
-  } else {
-    pg = PixelGrad{{0.f, 0.f, 0.f}, 0.f, 0.f, {0.f, 0.f, 0.f}, 0.f, 1.f};
-  }
+  bool hit;
+  int64_t pix;
+  const bool valid =
+      tile_pixel_ray(sv, cam, tile_begin, tile_stride, BWD_PER_TILE, BWD_THREADS, r, hit, pix);
+  const PixelGrad pg = pixel_grad(im, cfg, valid, pix);
   RayAccum acc;
   acc.init();
   float Y[9];
@@ -390,11 +384,120 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB) k_render_backward(
   const int ns = (int)cfg.n_s;
   WarpSmem& sm = smem[threadIdx.x >> 5];
   march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, [&](const Seg& seg, bool want) {
-    return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm, grad);
+    return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm,
+                            red_smem + (threadIdx.x >> 5) * RED_FLOATS, grad);
   });
 }
 
+// Logged backward: walks the warp's march-log chain (march_log.cuh).  Per
+// record: replay the compositing from the saved sums to form the adjoints,
+// then pass 2 over the saved candidate stream.  Warp layout = the forward's
+// (FWD_THREADS-thread CTAs, Z-order 8x4 blocks), so the records line up.
+#ifndef GSX_BWDL_THREADS
+#define GSX_BWDL_THREADS 128
+#endif
+#ifndef GSX_BWDL_MINB
+#define GSX_BWDL_MINB 4
+#endif
+constexpr int BWDL_THREADS = GSX_BWDL_THREADS;
+constexpr int BWDL_PER_TILE = 256 / BWDL_THREADS;
+
+__global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
+    k_render_backward_logged(SceneView sv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
+                             int64_t tile_stride, BwdImages im, const char* __restrict__ log,
+                             long long nw, float* __restrict__ grad) {
+  extern __shared__ float red_smem[];  // RED_FLOATS per warp
+  const long long wid = tile_warp_id(BWDL_PER_TILE, BWDL_THREADS);
+  if (!log_complete((void*)log, nw)[wid]) return;  // the replay kernel covers this warp
+  const int lane = threadIdx.x & 31;
+  RayCtx r;
+  bool hit;
+  int64_t pix;
+  const bool valid =
+      tile_pixel_ray(sv, cam, tile_begin, tile_stride, BWDL_PER_TILE, BWDL_THREADS, r, hit, pix);
+  const PixelGrad pg = pixel_grad(im, cfg, valid, pix);
+  RayAccum acc;
+  acc.init();
+  float Y[9];
+  sh_basis_f(r.df, Y);
+  float* red = red_smem + (threadIdx.x >> 5) * RED_FLOATS;
+  long long off = log_first((void*)log)[wid];
+  while (off >= 0) {
+    const long long start = off;
+    const LogRec* h = (const LogRec*)(log + off);
+    while (h->kind != 0) {
+      off = h->next;
+      h = (const LogRec*)(log + off);
+    }
+    const char* body = log + off + 128;
+    const double tb = ((const double*)body)[lane];
+    const double dt = ((const double*)body)[32 + lane];
+    const int mc = ((const int*)(body + 512))[lane];
+    const int mmax = h->mmax;
+    const long long next = h->next;
+    const float* smp = (const float*)(body + LOG_LANE_BYTES);
+    const float dtf = (float)dt;
+    float wos[16], hh[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      wos[j] = hh[j] = 0.f;
+      if (j < mmax && j < mc) {
+        const float Wj[3] = {smp[(4 * j + 1) * 32 + lane], smp[(4 * j + 2) * 32 + lane],
+                             smp[(4 * j + 3) * 32 + lane]};
+        sample_adjoint(acc, pg, smp[(4 * j) * 32 + lane], Wj, (float)(tb + (double)j * dt), dtf,
+                       wos[j], hh[j]);
+      }
+    }
+    const SegBase base = seg_base(r, tb);
+    const bool want = mc > 0;
+    // pass 2 over the record chain start..off
+    for (long long o = start;;) {
+      const LogRec* ho = (const LogRec*)(log + o);
+      const int count = ho->count;
+      const int32_t* list =
+          (const int32_t*)(log + o + 128 + (ho->kind == 0 ? LOG_LANE_BYTES + 512LL * mmax : 0));
+      for (int i0 = 0; i0 < count; i0 += 32) {
+        const int mine = i0 + lane < count ? list[i0 + lane] : 0;
+        const int nb = min(32, count - i0);
+        for (int k = 0; k < nb; ++k)
+          grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, mine, k), want, mc, base, dtf, Y, pg,
+                         wos, hh, red, grad);
+      }
+      if (o == off) break;
+      o = ho->next;
+    }
+    off = next;
+  }
+}
+
 }  // namespace
+
+constexpr int BWD_SMEM = (BWD_THREADS / 32) * RED_FLOATS * (int)sizeof(float);
+constexpr int BWDL_SMEM = (BWDL_THREADS / 32) * RED_FLOATS * (int)sizeof(float);
+
+static int bwd_smem_setup() {
+  static bool done = false;  // idempotent; the attribute is per function
+  if (done) return GSX_OK;
+  if (cudaFuncSetAttribute(k_render_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           BWD_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_render_backward_logged,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, BWDL_SMEM) != cudaSuccess)
+    return gsx_check_launch();
+  done = true;
+  return GSX_OK;
+}
+
+static int bwd_check(const gsx_render_cfg* cfg, const gsx_camera* cam, int64_t n,
+                     const BwdImages& im, const float* grad, int64_t tile_begin,
+                     int64_t tile_stride) {
+  int rc = gsx_validate_cfg(cfg);
+  if (rc) return rc;
+  if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
+  if (n <= 0) return GSX_ERR_EMPTY;
+  if (!im.rgb || !im.depth || !im.trans || !im.dL_drgb || !grad) return GSX_ERR_ARG;
+  if (tile_stride < 1 || tile_begin < 0) return GSX_ERR_ARG;
+  return GSX_OK;
+}
 
 extern "C" int gsx_render_backward(const void* scene_arena, const void* bvh_arena,
                                    const float* params, int64_t n, const gsx_camera* cam,
@@ -405,19 +508,48 @@ extern "C" int gsx_render_backward(const void* scene_arena, const void* bvh_aren
                                    gsx_dev_status* dev_status, void* stream) {
   (void)params;
   (void)dev_status;
-  int rc = gsx_validate_cfg(cfg);
+  const BwdImages im{rgb, depth, trans, dL_drgb, dL_ddepth, dL_dtrans};
+  int rc = bwd_check(cfg, cam, n, im, grad, tile_begin, tile_stride);
   if (rc) return rc;
-  if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
-  if (n <= 0) return GSX_ERR_EMPTY;
-  if (!rgb || !depth || !trans || !dL_drgb || !grad) return GSX_ERR_ARG;
-  if (tile_stride < 1 || tile_begin < 0) return GSX_ERR_ARG;
   int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
   if (tile_begin >= tiles) return GSX_OK;
   int64_t blocks = BWD_PER_TILE * ((tiles - tile_begin + tile_stride - 1) / tile_stride);
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
-  k_render_backward<<<(unsigned)blocks, BWD_THREADS, 0, (cudaStream_t)stream>>>(
-      sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, dL_drgb, dL_ddepth,
-      dL_dtrans, grad);
+  rc = bwd_smem_setup();
+  if (rc) return rc;
+  k_render_backward<<<(unsigned)blocks, BWD_THREADS, BWD_SMEM, (cudaStream_t)stream>>>(
+      sv, bv, *cam, *cfg, tile_begin, tile_stride, im, nullptr, grad);
+  return gsx_check_launch();
+}
+
+extern "C" int gsx_render_backward_logged(const void* scene_arena, const void* bvh_arena,
+                                          const float* params, int64_t n, const gsx_camera* cam,
+                                          const gsx_render_cfg* cfg, int64_t tile_begin,
+                                          int64_t tile_stride, const float* rgb,
+                                          const float* depth, const float* trans,
+                                          const float* dL_drgb, const float* dL_ddepth,
+                                          const float* dL_dtrans, const void* log, float* grad,
+                                          gsx_dev_status* dev_status, void* stream) {
+  (void)params;
+  (void)dev_status;
+  const BwdImages im{rgb, depth, trans, dL_drgb, dL_ddepth, dL_dtrans};
+  int rc = bwd_check(cfg, cam, n, im, grad, tile_begin, tile_stride);
+  if (rc) return rc;
+  if (!log) return GSX_ERR_ARG;
+  int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+  if (tile_begin >= tiles) return GSX_OK;
+  const int64_t ntl = (tiles - tile_begin + tile_stride - 1) / tile_stride;
+  const long long nw = 8 * ntl;
+  SceneView sv = scene_view((void*)scene_arena, n);
+  BvhView bv = bvh_view((void*)bvh_arena, n);
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = bwd_smem_setup();
+  if (rc) return rc;
+  k_render_backward_logged<<<(unsigned)(BWDL_PER_TILE * ntl), BWDL_THREADS, BWDL_SMEM, s>>>(
+      sv, *cam, *cfg, tile_begin, tile_stride, im, (const char*)log, nw, grad);
+  // warps whose records overflowed the arena: full replay
+  k_render_backward<<<(unsigned)(BWD_PER_TILE * ntl), BWD_THREADS, BWD_SMEM, s>>>(
+      sv, bv, *cam, *cfg, tile_begin, tile_stride, im, log_complete((void*)log, nw), grad);
   return gsx_check_launch();
 }

@@ -3,6 +3,12 @@
 #pragma once
 #include "gsx_common.cuh"
 
+// Rarely-taken per-lane paths (closest hit, phantom probe) are kept out of
+// line: the march kernels are instruction-cache sensitive.
+#ifndef GSX_COLD
+#define GSX_COLD __noinline__
+#endif
+
 namespace gsx {
 
 // ---------------------------------------------------------------------------
@@ -344,7 +350,9 @@ __device__ inline bool traverse_segment(const BvhView& bv, const RayCtx& r, floa
 // closest ellipsoid entry in [t_lo, t_hi] (spatial.py:309-354): fp32 node
 // tests with margin, near child first, pruning by the current best; leaves
 // use the fp64 Kahan interval in the primitive's unit-sphere frame.
-__device__ inline bool closest_hit_r(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+// Cold path (about 2 calls per ray): kept out of line so the hot march loops
+// stay compact in the instruction cache.
+static __device__ GSX_COLD bool closest_hit_r(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                      double t_lo, double t_hi, double& hit, uint32_t& visits) {
   if (t_lo > t_hi) return false;
   double best = INFINITY;

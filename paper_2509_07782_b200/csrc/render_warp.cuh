@@ -294,7 +294,7 @@ __device__ inline void accumulate_list(const SceneView& sv, const RayCtx& r, con
 // Exact AABB-emptiness of the lane's segment (reference semantics) after the
 // true-intersection pass; STATS additionally counts every exact overlap.
 template <bool STATS>
-__device__ inline void emptiness_tail(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                       bool want, const Seg& seg, bool& nonempty,
                                       Counters<STATS>& cnt) {
   PH_BEGIN(ph_ph)

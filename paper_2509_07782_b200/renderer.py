@@ -24,12 +24,61 @@ def _out(shape, out, device):
     return torch.empty(shape, dtype=torch.float32, device=device)
 
 
+class MarchLog:
+    """Device arena for the training forward's march log (include/gsx.h):
+    the forward records each warp's candidate lists and per-sample sums, the
+    backward consumes them instead of replaying the march.  Any capacity is
+    correct (warps that do not fit are replayed); `usage()` reports what the
+    last forward needed so `ensure()` can grow the arena."""
+
+    def __init__(self, camera: Camera, *, tile_begin: int = 0, tile_stride: int = 1,
+                 capacity: int | None = None, device="cuda"):
+        import ctypes
+
+        L = _lib.lib()
+        self.tile_begin, self.tile_stride = int(tile_begin), int(tile_stride)
+        cam_c = camera.to_c()
+        self.min_bytes = int(L.gsx_march_log_min_bytes(ctypes.byref(cam_c), self.tile_begin,
+                                                       self.tile_stride))
+        if self.min_bytes < 0:
+            raise ValueError("invalid camera / tile set for a march log")
+        if capacity is None:  # C2 measured ~5 KiB per ray; 8 KiB leaves headroom
+            rays = camera.width * camera.height // self.tile_stride
+            capacity = self.min_bytes + 8192 * rays
+        self.device = device
+        self.arena = torch.empty(max(int(capacity), self.min_bytes), dtype=torch.uint8,
+                                 device=device)
+
+    @property
+    def capacity(self) -> int:
+        return self.arena.numel()
+
+    def usage(self, stream=None):
+        """(bytes the last logged forward needed, overflowed?) -- synchronizes."""
+        import ctypes
+
+        used, ovf = ctypes.c_int64(0), ctypes.c_int(0)
+        check(_lib.lib().gsx_march_log_usage(ptr(self.arena), ctypes.byref(used),
+                                             ctypes.byref(ovf), stream_ptr(stream)),
+              "march_log_usage")
+        return int(used.value), bool(ovf.value)
+
+    def ensure(self, headroom: float = 1.25, stream=None) -> bool:
+        """Grow the arena if the last forward overflowed it; True if grown."""
+        used, ovf = self.usage(stream)
+        if not ovf:
+            return False
+        self.arena = torch.empty(int(used * headroom), dtype=torch.uint8, device=self.device)
+        return True
+
+
 def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin: int = 0,
            tile_stride: int = 1, rgb=None, depth=None, trans=None, stats: bool = False,
-           stream=None):
+           log: MarchLog | None = None, stream=None):
     """Render the 16x16 tiles tile_begin + k*tile_stride of `camera` into
     rgb [H,W,3], depth [H,W], trans [H,W] float32 CUDA tensors (allocated
-    unless given).  Returns (rgb, depth, trans, stats_tensor_or_None)."""
+    unless given).  Returns (rgb, depth, trans, stats_tensor_or_None).
+    With `log` (training) the march is also recorded for render_backward."""
     cfg = cfg or RenderConfig()
     L = _lib.lib()
     H, W = camera.height, camera.width
@@ -41,6 +90,17 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
     cam_c, cfg_c = camera.to_c(), cfg.to_c()
     import ctypes
 
+    if log is not None:
+        if stats:
+            raise ValueError("stats and log are exclusive")
+        if (log.tile_begin, log.tile_stride) != (int(tile_begin), int(tile_stride)):
+            raise ValueError("march log was sized for another tile set")
+        check(L.gsx_render_forward_logged(ptr(scene.arena), ptr(scene.bvh_arena), scene.n,
+                                          ctypes.byref(cam_c), ctypes.byref(cfg_c),
+                                          int(tile_begin), int(tile_stride), ptr(rgb),
+                                          ptr(depth), ptr(trans), ptr(log.arena), log.capacity,
+                                          None, stream_ptr(stream)), "render_forward_logged")
+        return rgb, depth, trans, None
     check(L.gsx_render_forward(ptr(scene.arena), ptr(scene.bvh_arena), scene.n,
                                ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
                                int(tile_stride), ptr(rgb), ptr(depth), ptr(trans), ptr(st), None,
@@ -50,11 +110,12 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
 
 def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans, dL_drgb,
                     dL_ddepth=None, dL_dtrans=None, *, grad=None, tile_begin: int = 0,
-                    tile_stride: int = 1, stream=None):
+                    tile_stride: int = 1, log: MarchLog | None = None, stream=None):
     """Backward of `render` (no reference counterpart):
     accumulates dL/d(records) into grad [N,87] float32 (record layout, storage
     order; allocated zeroed unless given).  rgb/depth/trans are the forward
-    outputs of the same tiles; dL_d* are the upstream gradients (CUDA tensors)."""
+    outputs of the same tiles; dL_d* are the upstream gradients (CUDA tensors).
+    `log` = the MarchLog the forward of these outputs wrote (skips the replay)."""
     import ctypes
 
     cfg = cfg or RenderConfig()
@@ -63,6 +124,16 @@ def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans,
         grad = torch.zeros((scene.n, 87), dtype=torch.float32, device=scene.device)
     cam_c, cfg_c = camera.to_c(), cfg.to_c()
     c = lambda t: None if t is None else t.contiguous()  # noqa: E731
+    if log is not None:
+        if (log.tile_begin, log.tile_stride) != (int(tile_begin), int(tile_stride)):
+            raise ValueError("march log was recorded for another tile set")
+        check(L.gsx_render_backward_logged(
+            ptr(scene.arena), ptr(scene.bvh_arena), ptr(scene.params), scene.n,
+            ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin), int(tile_stride),
+            ptr(c(rgb)), ptr(c(depth)), ptr(c(trans)), ptr(c(dL_drgb)), ptr(c(dL_ddepth)),
+            ptr(c(dL_dtrans)), ptr(log.arena), ptr(grad), None, stream_ptr(stream)),
+            "render_backward_logged")
+        return grad
     check(L.gsx_render_backward(ptr(scene.arena), ptr(scene.bvh_arena), ptr(scene.params), scene.n,
                                 ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
                                 int(tile_stride), ptr(c(rgb)), ptr(c(depth)), ptr(c(trans)),

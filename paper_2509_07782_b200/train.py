@@ -26,7 +26,7 @@ from . import _lib
 from ._lib import check, ptr, stream_ptr
 from .config import Camera, RenderConfig
 from .loss import ImageLoss, IsoLossConfig, LossConfig
-from .renderer import render, render_backward
+from .renderer import MarchLog, render, render_backward
 
 # default per-slot learning rates of the 87-float record
 LR_GROUPS = {"mean": (0, 3, 1e-4), "quat": (3, 7, 1e-3), "scale": (7, 10, 1e-4),
@@ -99,7 +99,7 @@ class Trainer:
 
     def __init__(self, scene, camera: Camera, cfg: RenderConfig | None = None,
                  loss_cfg: LossConfig = LossConfig(), iso_cfg: IsoLossConfig = IsoLossConfig(),
-                 lr=None, group=None):
+                 lr=None, group=None, march_log: bool = True):
         import torch.distributed as dist
 
         self.scene, self.camera = scene, camera
@@ -120,6 +120,10 @@ class Trainer:
         self.loss = ImageLoss(H, W, 3, dev)
         self.adam = Adam(scene.params, scene.sigma_eps, lr)
         self._iso = torch.zeros(1, dtype=torch.float64, device=dev)
+        # the forward records its march for the backward (renderer.MarchLog)
+        self.log = (MarchLog(camera, tile_begin=self.rank, tile_stride=self.world, device=dev)
+                    if march_log else None)
+        self._steps = 0
 
     def step(self, target, want_loss: bool = False):
         """One optimization step against `target` [H,W,3] (CUDA).  Returns the
@@ -132,19 +136,23 @@ class Trainer:
             self.depth.zero_()
             self.trans.zero_()
         render(s, self.camera, self.cfg, tile_begin=self.rank, tile_stride=self.world,
-               rgb=self.rgb, depth=self.depth, trans=self.trans)
+               rgb=self.rgb, depth=self.depth, trans=self.trans, log=self.log)
         assemble_tiles([self.rgb, self.depth, self.trans], self.group)
         vals, _ = self.loss(self.rgb, target, self.loss_cfg.mix, grad=self.dI,
                             want_value=want_loss)
         self.grad.zero_()
         render_backward(s, self.camera, self.cfg, self.rgb, self.depth, self.trans, self.dI,
-                        grad=self.grad, tile_begin=self.rank, tile_stride=self.world)
+                        grad=self.grad, tile_begin=self.rank, tile_stride=self.world,
+                        log=self.log)
         if self.rank == 0 and self.iso_cfg.lambda_s > 0:
             check(L.gsx_iso_loss(ptr(s.params), s.n, float(self.iso_cfg.r0),
                                  float(self.iso_cfg.lambda_s), ptr(self.grad), ptr(self._iso),
                                  stream_ptr()), "iso_loss")
         allreduce_grad(self.grad, self.group)
         self.adam.step(self.grad)
+        self._steps += 1
+        if self.log is not None and (self._steps == 1 or want_loss):
+            self.log.ensure()  # overflowed warps were replayed; size up for the next step
         if want_loss:
             iso = float(self._iso.item()) / s.n if self.rank == 0 else 0.0
             return vals[0] + self.iso_cfg.lambda_s * iso

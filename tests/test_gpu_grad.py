@@ -28,19 +28,37 @@ def _compare(g_gpu, g_ref, tol_l2=1e-3, tol_max=2e-3):
         assert errmax <= tol_max * np.abs(B).max() + floor_max, (g, errmax, np.abs(B).max())
 
 
-def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True):
+def _march_log(G, scene, cam, cfg, log):
+    """MarchLog for mode 'full' (fits), 'tiny' (no warp fits: every warp is
+    replayed) or 'partial' (some warps fit, the rest are replayed)."""
+    if log is None:
+        return None
+    if log == "full":
+        return G.MarchLog(cam)
+    probe = G.MarchLog(cam)
+    G.render(scene, cam, cfg, log=probe)
+    used, ovf = probe.usage()
+    assert not ovf and used > probe.min_bytes
+    cap = probe.min_bytes if log == "tiny" else (probe.min_bytes + used) // 2
+    return G.MarchLog(cam, capacity=cap)
+
+
+def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None):
     import torch
 
     scene = G.Scene.from_records(rec, sigma_eps=eps)
     cfg = G.RenderConfig(**cfg_kw)
-    rgb, depth, trans, _ = G.render(scene, cam, cfg)
+    lg = _march_log(G, scene, cam, cfg, log)
+    rgb, depth, trans, _ = G.render(scene, cam, cfg, log=lg)
+    if lg is not None:
+        assert lg.usage()[1] == (log != "full")
     rng = np.random.default_rng(seed)
     H, W = cam.height, cam.width
     gC = rng.normal(size=(H, W, 3))
     gD = 0.1 * rng.normal(size=(H, W)) if with_depth else np.zeros((H, W))
     gT = rng.normal(size=(H, W))
     t = lambda a: torch.as_tensor(a, dtype=torch.float32, device="cuda")  # noqa: E731
-    grad = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT))
+    grad = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg)
     osc = O.OracleScene(rec, eps)
     rays = O.camera_rays(cam.center, cam.quat, cam.focal, W, H)
     R, T, D, gref = osc.backward_rays(rays, O.OCfg.make(**cfg_kw), gC.reshape(-1, 3),
@@ -78,4 +96,28 @@ def test_backward_c1_adaptive():
                                              base_scale=0.01177))
     cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=32, height=32)[0]
     g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive"))
+    _compare(g, gref)
+
+
+@pytest.mark.parametrize("log", ["full", "tiny", "partial"])
+@pytest.mark.parametrize("mode", ["uniform", "adaptive"])
+def test_backward_march_log(mode, log):
+    """Logged forward + logged backward (march_log.cuh), including arenas too
+    small for some / all warps (those warps fall back to the replay kernel)."""
+    import paper_2509_07782_b200 as G
+
+    rec = f32_records(gen_test_scene_records("random-cloud", count=300, seed=4, anisotropy=3.0,
+                                             base_scale=0.05))
+    cam = G.orbit_cameras(2, radius=3.0, focal=40.0, width=40, height=24)[1]
+    g, gref = _run(G, rec, 0.01, cam, dict(mode=mode, background=(0.2, 0.5, 0.9)), log=log)
+    _compare(g, gref)
+
+
+def test_backward_march_log_c1():
+    import paper_2509_07782_b200 as G
+
+    rec = f32_records(gen_test_scene_records("random-cloud", 10_000, seed=0, anisotropy=3.0,
+                                             base_scale=0.01177))
+    cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=32, height=32)[0]
+    g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive"), log="full")
     _compare(g, gref)
