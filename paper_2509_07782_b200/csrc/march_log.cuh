@@ -31,7 +31,8 @@ struct LogHeader {
   unsigned long long cap;   // arena bytes
   unsigned int overflow;
   unsigned int nwarps;
-  unsigned int pad[26];
+  unsigned long long need;  // bytes every record would need (incl. those that did not fit)
+  unsigned int pad[24];
 };
 static_assert(sizeof(LogHeader) == 128, "LogHeader is one 128-byte line");
 
@@ -68,6 +69,7 @@ struct LogWriter {
   char* base;
   long long first, prev;
   long long wid;
+  long long need;  // bytes this warp's records need, logged or not
   bool on;
 };
 
@@ -77,6 +79,7 @@ __device__ inline LogWriter log_writer(void* base, long long wid) {
   w.first = -1;
   w.prev = -1;
   w.wid = wid;
+  w.need = 0;
   w.on = base != nullptr;
   return w;
 }
@@ -84,6 +87,8 @@ __device__ inline LogWriter log_writer(void* base, long long wid) {
 // Allocate `bytes` for this warp and link it after the warp's previous record.
 // Warp-uniform; returns the offset, or -1 (and turns the writer off) on overflow.
 __device__ inline long long log_alloc(LogWriter& w, long long bytes) {
+  w.need += bytes;
+  if (!w.on) return -1;
   const int lane = threadIdx.x & 31;
   LogHeader* h = (LogHeader*)w.base;
   long long off = 0;
@@ -117,13 +122,15 @@ __device__ inline void log_header(const LogWriter& w, long long off, int count, 
   }
 }
 
+// The log streams through L2 once each way: evict-first stores/loads keep
+// the scene and BVH resident.
 __device__ inline void log_list(int32_t* dst, const int32_t* list, int count) {
-  for (int i = threadIdx.x & 31; i < count; i += 32) dst[i] = list[i];
+  for (int i = threadIdx.x & 31; i < count; i += 32) __stcs(dst + i, list[i]);
 }
 
 // kind 1: a full shared-list chunk of a long candidate stream
 __device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int count) {
-  if (!w.on) return;
+  if (!w.base) return;
   const long long off = log_alloc(w, 128 + log_round128(4LL * count));
   if (off < 0) return;
   log_header(w, off, count, 1, 0);
@@ -134,7 +141,7 @@ __device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int cou
 __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, double tb,
                                 double dt, int mc, const float (&sig)[16],
                                 const float (&W)[16][3]) {
-  if (!w.on) return;
+  if (!w.base) return;
   const int lane = threadIdx.x & 31;
   const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
   const long long off =
@@ -142,18 +149,18 @@ __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, do
   if (off < 0) return;
   log_header(w, off, count, 0, mmax);
   char* body = w.base + off + 128;
-  ((double*)body)[lane] = tb;
-  ((double*)body)[32 + lane] = dt;
-  ((int*)(body + 512))[lane] = mc;
+  __stcs((double*)body + lane, tb);
+  __stcs((double*)body + 32 + lane, dt);
+  __stcs((int*)(body + 512) + lane, mc);
   float* smp = (float*)(body + LOG_LANE_BYTES);
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j < mmax) {
       const bool in = j < mc;
-      smp[(4 * j + 0) * 32 + lane] = in ? sig[j] : 0.f;
-      smp[(4 * j + 1) * 32 + lane] = in ? W[j][0] : 0.f;
-      smp[(4 * j + 2) * 32 + lane] = in ? W[j][1] : 0.f;
-      smp[(4 * j + 3) * 32 + lane] = in ? W[j][2] : 0.f;
+      __stcs(smp + (4 * j + 0) * 32 + lane, in ? sig[j] : 0.f);
+      __stcs(smp + (4 * j + 1) * 32 + lane, in ? W[j][0] : 0.f);
+      __stcs(smp + (4 * j + 2) * 32 + lane, in ? W[j][1] : 0.f);
+      __stcs(smp + (4 * j + 3) * 32 + lane, in ? W[j][2] : 0.f);
     }
   }
   log_list((int32_t*)(body + LOG_LANE_BYTES + 512LL * mmax), list, count);
@@ -164,6 +171,14 @@ __device__ inline void log_finish(const LogWriter& w, long long nw) {
   if (!w.base || (threadIdx.x & 31) != 0) return;
   log_first(w.base)[w.wid] = w.on ? w.first : -1;
   log_complete(w.base, nw)[w.wid] = w.on ? 1u : 0u;
+  atomicAdd(&((LogHeader*)w.base)->need, (unsigned long long)w.need);
+}
+
+// L2 prefetch of a record's first `bytes` (the warp's next record, issued
+// while the current one is processed)
+__device__ inline void log_prefetch(const char* p, long long bytes) {
+  for (long long o = (long long)(threadIdx.x & 31) * 128; o < bytes; o += 32 * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
 }
 
 }  // namespace gsx

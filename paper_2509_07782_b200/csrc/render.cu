@@ -265,6 +265,7 @@ __global__ void k_log_init(LogHeader* h, unsigned long long cap, unsigned nw, lo
   h->cap = cap;
   h->overflow = 0;
   h->nwarps = nw;
+  h->need = (unsigned long long)table;
 }
 
 extern "C" int64_t gsx_march_log_min_bytes(const gsx_camera* cam, int64_t tile_begin,
@@ -309,7 +310,7 @@ extern "C" int gsx_march_log_usage(const void* log, int64_t* used_bytes, int* ov
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_CHECK_RET(cudaMemcpyAsync(&h, log, sizeof h, cudaMemcpyDeviceToHost, s));
   CUDA_CHECK_RET(cudaStreamSynchronize(s));
-  if (used_bytes) *used_bytes = (int64_t)h.head;
+  if (used_bytes) *used_bytes = (int64_t)h.need;
   if (overflow) *overflow = (int)h.overflow;
   return GSX_OK;
 }

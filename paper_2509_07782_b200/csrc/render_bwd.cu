@@ -430,11 +430,12 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
       h = (const LogRec*)(log + off);
     }
     const char* body = log + off + 128;
-    const double tb = ((const double*)body)[lane];
-    const double dt = ((const double*)body)[32 + lane];
-    const int mc = ((const int*)(body + 512))[lane];
+    const double tb = __ldcs((const double*)body + lane);
+    const double dt = __ldcs((const double*)body + 32 + lane);
+    const int mc = __ldcs((const int*)(body + 512) + lane);
     const int mmax = h->mmax;
     const long long next = h->next;
+    if (next >= 0) log_prefetch(log + next, 128 + LOG_LANE_BYTES + 512 * 16);
     const float* smp = (const float*)(body + LOG_LANE_BYTES);
     const float dtf = (float)dt;
     float wos[16], hh[16];
@@ -442,10 +443,11 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     for (int j = 0; j < 16; ++j) {
       wos[j] = hh[j] = 0.f;
       if (j < mmax && j < mc) {
-        const float Wj[3] = {smp[(4 * j + 1) * 32 + lane], smp[(4 * j + 2) * 32 + lane],
-                             smp[(4 * j + 3) * 32 + lane]};
-        sample_adjoint(acc, pg, smp[(4 * j) * 32 + lane], Wj, (float)(tb + (double)j * dt), dtf,
-                       wos[j], hh[j]);
+        const float Wj[3] = {__ldcs(smp + (4 * j + 1) * 32 + lane),
+                             __ldcs(smp + (4 * j + 2) * 32 + lane),
+                             __ldcs(smp + (4 * j + 3) * 32 + lane)};
+        sample_adjoint(acc, pg, __ldcs(smp + (4 * j) * 32 + lane), Wj,
+                       (float)(tb + (double)j * dt), dtf, wos[j], hh[j]);
       }
     }
     const SegBase base = seg_base(r, tb);
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
       const int32_t* list =
           (const int32_t*)(log + o + 128 + (ho->kind == 0 ? LOG_LANE_BYTES + 512LL * mmax : 0));
       for (int i0 = 0; i0 < count; i0 += 32) {
-        const int mine = i0 + lane < count ? list[i0 + lane] : 0;
+        const int mine = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
         const int nb = min(32, count - i0);
         for (int k = 0; k < nb; ++k)
           grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, mine, k), want, mc, base, dtf, Y, pg,

@@ -33,13 +33,11 @@ def _march_log(G, scene, cam, cfg, log):
     replayed) or 'partial' (some warps fit, the rest are replayed)."""
     if log is None:
         return None
-    if log == "full":
-        return G.MarchLog(cam)
-    probe = G.MarchLog(cam)
+    probe = G.MarchLog(cam, capacity=1 << 28)
     G.render(scene, cam, cfg, log=probe)
     used, ovf = probe.usage()
     assert not ovf and used > probe.min_bytes
-    cap = probe.min_bytes if log == "tiny" else (probe.min_bytes + used) // 2
+    cap = {"full": used, "tiny": probe.min_bytes, "partial": (probe.min_bytes + used) // 2}[log]
     return G.MarchLog(cam, capacity=cap)
 
 
