@@ -12,10 +12,13 @@
 //
 // Arena (all offsets in bytes from the arena base, 128-byte aligned):
 //   [LogHeader, 128 B][int64 first[nw]][uint32 complete[nw]] [records ...]
-// Record = 128-byte LogRec header + body:
-//   kind 0 (full):  double tb[32], double dt[32], int32 mc[32],
-//                   float smp[mmax][4][32] (sigma, W0, W1, W2 per sample/lane),
-//                   int32 list[count]
+// Record = 128-byte LogRec header + body.  Only the lanes with samples in
+// this iteration (`act` ballot; the depth-synchronous schedule leaves most
+// lanes waiting in most iterations) are stored, in slot order
+// slot = popc(act & lanes below):
+//   kind 0 (full):  double tb[nact], double dt[nact], int32 mc[nact],
+//                   float4 smp[mmax][nact] (sigma, W0, W1, W2), int32 list[count]
+//                   (each array 16-byte aligned, see LogLayout)
 //   kind 1 (list):  int32 list[count]   (a leading chunk of a candidate stream
 //                   longer than the shared list; the kind-0 record that
 //                   follows holds the rest and the sample sums)
@@ -40,14 +43,26 @@ struct LogRec {
   long long next;  // offset of the warp's next record, -1 = last
   int count;       // list entries in this record
   int kind;        // 0 full, 1 list chunk
-  int mmax;        // samples stored per lane (warp max of mc), kind 0
-  int pad[27];
+  int mmax;        // samples stored per active lane (warp max of mc), kind 0
+  unsigned act;    // lanes stored (mc > 0), kind 0
+  int pad[26];
 };
 static_assert(sizeof(LogRec) == 128, "LogRec is one 128-byte line");
 
-constexpr long long LOG_LANE_BYTES = 32 * 8 + 32 * 8 + 32 * 4;  // tb, dt, mc
-
 __host__ __device__ inline long long log_round128(long long x) { return (x + 127) & ~127LL; }
+__host__ __device__ inline long long log_round16(long long x) { return (x + 15) & ~15LL; }
+
+// byte offsets inside a kind-0 body for nact stored lanes
+struct LogLayout {
+  long long dt, mc, smp, list, bytes;
+  __host__ __device__ LogLayout(int nact, int mmax, int count) {
+    dt = 8LL * nact;
+    mc = 16LL * nact;
+    smp = log_round16(20LL * nact);
+    list = smp + 16LL * nact * mmax;
+    bytes = 128 + log_round128(list + 4LL * count);
+  }
+};
 __host__ __device__ inline long long log_table_bytes(long long nw) {
   return log_round128(128 + 8 * nw) + log_round128(4 * nw);
 }
@@ -112,13 +127,14 @@ __device__ inline long long log_alloc(LogWriter& w, long long bytes) {
 }
 
 __device__ inline void log_header(const LogWriter& w, long long off, int count, int kind,
-                                  int mmax) {
+                                  int mmax, unsigned act) {
   if ((threadIdx.x & 31) == 0) {
     LogRec* r = (LogRec*)(w.base + off);
     r->next = -1;
     r->count = count;
     r->kind = kind;
     r->mmax = mmax;
+    r->act = act;
   }
 }
 
@@ -133,37 +149,39 @@ __device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int cou
   if (!w.base) return;
   const long long off = log_alloc(w, 128 + log_round128(4LL * count));
   if (off < 0) return;
-  log_header(w, off, count, 1, 0);
+  log_header(w, off, count, 1, 0, 0u);
   log_list((int32_t*)(w.base + off + 128), list, count);
 }
 
-// kind 0: the lane block, the per-sample sums and the last list chunk
+// kind 0: the active lanes' block, their per-sample sums, the last list chunk
 __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, double tb,
                                 double dt, int mc, const float (&sig)[16],
                                 const float (&W)[16][3]) {
   if (!w.base) return;
   const int lane = threadIdx.x & 31;
+  const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
+  const int nact = __popc(act);
   const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
-  const long long off =
-      log_alloc(w, 128 + LOG_LANE_BYTES + 512LL * mmax + log_round128(4LL * count));
+  const LogLayout L(nact, mmax, count);
+  const long long off = log_alloc(w, L.bytes);
   if (off < 0) return;
-  log_header(w, off, count, 0, mmax);
+  log_header(w, off, count, 0, mmax, act);
   char* body = w.base + off + 128;
-  __stcs((double*)body + lane, tb);
-  __stcs((double*)body + 32 + lane, dt);
-  __stcs((int*)(body + 512) + lane, mc);
-  float* smp = (float*)(body + LOG_LANE_BYTES);
+  if (mc > 0) {
+    const int slot = __popc(act & ((1u << lane) - 1u));
+    __stcs((double*)body + slot, tb);
+    __stcs((double*)(body + L.dt) + slot, dt);
+    __stcs((int*)(body + L.mc) + slot, mc);
+    float4* smp = (float4*)(body + L.smp) + slot;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < mmax) {
-      const bool in = j < mc;
-      __stcs(smp + (4 * j + 0) * 32 + lane, in ? sig[j] : 0.f);
-      __stcs(smp + (4 * j + 1) * 32 + lane, in ? W[j][0] : 0.f);
-      __stcs(smp + (4 * j + 2) * 32 + lane, in ? W[j][1] : 0.f);
-      __stcs(smp + (4 * j + 3) * 32 + lane, in ? W[j][2] : 0.f);
+    for (int j = 0; j < 16; ++j) {
+      if (j < mmax)
+        __stcs(smp + (long long)j * nact,
+               j < mc ? make_float4(sig[j], W[j][0], W[j][1], W[j][2])
+                      : make_float4(0.f, 0.f, 0.f, 0.f));
     }
   }
-  log_list((int32_t*)(body + LOG_LANE_BYTES + 512LL * mmax), list, count);
+  log_list((int32_t*)(body + L.list), list, count);
 }
 
 // end of the warp: publish its chain head and whether it is complete

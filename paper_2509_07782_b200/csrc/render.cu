@@ -81,12 +81,8 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
     // front-to-back compositing (renderer.py:230-239); zero-density samples
     // leave the state unchanged, so compositing an empty segment is a no-op
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j < mc) {
-        float tj = (float)(tb + (double)j * seg.dt);
-        acc.add_sample(sig[j], W[j], tj, dtf);
-      }
-    }
+    for (int j = 0; j < 16; ++j)
+      acc.add_sample(j < mc ? sig[j] : 0.f, W[j], (float)(tb + (double)j * seg.dt), dtf);
     PH_END(3, ph_c)
   }
   if (STATS) cnt.visits += visits;

@@ -430,24 +430,31 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
       h = (const LogRec*)(log + off);
     }
     const char* body = log + off + 128;
-    const double tb = __ldcs((const double*)body + lane);
-    const double dt = __ldcs((const double*)body + 32 + lane);
-    const int mc = __ldcs((const int*)(body + 512) + lane);
+    const unsigned act = h->act;
     const int mmax = h->mmax;
     const long long next = h->next;
-    if (next >= 0) log_prefetch(log + next, 128 + LOG_LANE_BYTES + 512 * 16);
-    const float* smp = (const float*)(body + LOG_LANE_BYTES);
+    const LogLayout Lo(__popc(act), mmax, h->count);
+    if (next >= 0) log_prefetch(log + next, 128 + Lo.list);
+    const bool mine = (act >> lane) & 1u;
+    const int slot = __popc(act & ((1u << lane) - 1u));
+    double tb = 0.0, dt = 0.0;
+    int mc = 0;
+    if (mine) {
+      tb = __ldcs((const double*)body + slot);
+      dt = __ldcs((const double*)(body + Lo.dt) + slot);
+      mc = __ldcs((const int*)(body + Lo.mc) + slot);
+    }
+    const float4* smp = (const float4*)(body + Lo.smp) + slot;
+    const int nact = __popc(act);
     const float dtf = (float)dt;
     float wos[16], hh[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       wos[j] = hh[j] = 0.f;
       if (j < mmax && j < mc) {
-        const float Wj[3] = {__ldcs(smp + (4 * j + 1) * 32 + lane),
-                             __ldcs(smp + (4 * j + 2) * 32 + lane),
-                             __ldcs(smp + (4 * j + 3) * 32 + lane)};
-        sample_adjoint(acc, pg, __ldcs(smp + (4 * j) * 32 + lane), Wj,
-                       (float)(tb + (double)j * dt), dtf, wos[j], hh[j]);
+        const float4 v = __ldcs(smp + (long long)j * nact);
+        const float Wj[3] = {v.y, v.z, v.w};
+        sample_adjoint(acc, pg, v.x, Wj, (float)(tb + (double)j * dt), dtf, wos[j], hh[j]);
       }
     }
     const SegBase base = seg_base(r, tb);
@@ -456,13 +463,12 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     for (long long o = start;;) {
       const LogRec* ho = (const LogRec*)(log + o);
       const int count = ho->count;
-      const int32_t* list =
-          (const int32_t*)(log + o + 128 + (ho->kind == 0 ? LOG_LANE_BYTES + 512LL * mmax : 0));
+      const int32_t* list = (const int32_t*)(log + o + 128 + (ho->kind == 0 ? Lo.list : 0));
       for (int i0 = 0; i0 < count; i0 += 32) {
-        const int mine = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
+        const int ent = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
         const int nb = min(32, count - i0);
         for (int k = 0; k < nb; ++k)
-          grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, mine, k), want, mc, base, dtf, Y, pg,
+          grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), want, mc, base, dtf, Y, pg,
                          wos, hh, red, grad);
       }
       if (o == off) break;
