@@ -52,17 +52,21 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       W[j][0] = W[j][1] = W[j][2] = 0.f;
     }
     if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
-    // n_s > 16 processes the segment in 16-sample chunks, each with its own traversal
-    WarpTrav st;
-    SegLimits lim;
-    int count;
-    stage_candidates(bv, r, want, seg, sm, st, count, lim, visits);
+    // n_s > 16 processes the segment in 16-sample chunks, each with its own
+    // traversal.  One traversal call site: list chunks of LCAP entries are
+    // traversed, then accumulated, until the stream is exhausted.
+    const SegLimits lim = seg_limits(r, seg);
+    WarpTrav st{0, 0, false, false};
+    int count = 0;
     const bool save = SAVE && __any_sync(FULL, want && mc > 0);
     auto exact = [&](int64_t p) {
       if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
     };
     for (;;) {
+      PH_BEGIN(ph_t)
+      warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+      PH_END(1, ph_t)
       PH_BEGIN(ph_p)
       accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
       PH_END(2, ph_p)
@@ -70,7 +74,6 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       if (save) log_list_chunk(lw, sm.list, count);
       __syncwarp();
       count = 0;
-      warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
     }
     if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
     if (STATS) {

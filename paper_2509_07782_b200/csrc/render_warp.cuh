@@ -286,6 +286,8 @@ __device__ inline void accumulate_list(const SceneView& sv, const RayCtx& r, con
                                        int count, bool want, int mc, const SegBase& base,
                                        float dtf, const float* Y, float (&sig)[16],
                                        float (&W)[16][3], Pre&& pre) {
+  // (L1 prefetch of the listed geometry / appearance blocks measured slower:
+  // 40.9 vs 40.0 ms on C3 -- the entry loop is not load-latency bound)
   for (int i = 0; i < count; ++i) {
     const int64_t p = sm.list[i];
     pre(p);
@@ -345,27 +347,32 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
   bool active = hit;
   uint32_t visits = 0;
   PH_BEGIN(ph_all)
-  PH_BEGIN(ph_ch0)
-  if (active) {
-    if (uniform) {
-      n_seg = (long long)ceil((t_f - t_n) / ds_u);
-      if (n_seg < 1) n_seg = 1;
-    }
-    if (cfg.ess) {
+  if (active && uniform) {
+    n_seg = (long long)ceil((t_f - t_n) / ds_u);
+    if (n_seg < 1) n_seg = 1;
+  }
+  // ESS closest-hit requests -- the initial one from t_n and the restart after
+  // every empty segment -- are served at one call site at the top of the loop
+  // (one inlined copy of the traversal instead of two)
+  bool need_ch = active && cfg.ess, first_ch = true;
+  double ch_from = t_n;
+  while (__any_sync(FULL, active)) {
+    PH_BEGIN(ph_ch)
+    if (need_ch) {
       double h;
       if (STATS) cnt.ch_calls++;
-      if (!closest_hit_r(sv, bv, r, t_n, t_f, h, visits)) {
+      if (!closest_hit_r(sv, bv, r, ch_from, t_f, h, visits)) {
         active = false;
       } else if (uniform) {
-        long long kk = (long long)((h - t_n) / ds_u);
-        k = kk > 0 ? kk : 0;
+        const long long kk = (long long)((h - t_n) / ds_u), kmin = first_ch ? 0 : k + 1;
+        k = kk > kmin ? kk : kmin;
       } else {
-        t_s = h;
+        t_s = h;  // adaptive mode has no global grid: restart here
       }
+      need_ch = false;
+      first_ch = false;
     }
-  }
-  PH_END(0, ph_ch0)
-  while (__any_sync(FULL, active)) {
+    PH_END(0, ph_ch)
     if (active) {
       if (uniform)
         active = k < n_seg && acc.transmittance() > cfg.t_eps;
@@ -426,16 +433,8 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
       } else {
         if (STATS) cnt.skipped++;
         if (cfg.ess) {
-          double h;
-          if (STATS) cnt.ch_calls++;
-          if (!closest_hit_r(sv, bv, r, seg.t1, t_f, h, visits)) {
-            active = false;
-          } else if (uniform) {
-            long long kk = (long long)((h - t_n) / ds_u);
-            k = kk > k + 1 ? kk : k + 1;
-          } else {
-            t_s = h;  // adaptive mode has no global grid: restart here
-          }
+          need_ch = true;  // served at the top of the next iteration
+          ch_from = seg.t1;
         } else {
           if (STATS) cnt.samples += seg.m;
           if (uniform)
