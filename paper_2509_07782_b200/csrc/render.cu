@@ -118,14 +118,16 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
   });
 }
 
-// CTA = FWD_THREADS rays = 256 / FWD_THREADS CTAs per 16x16 tile.  Measured on
-// C3 (ms/frame): 256x2 45.9, 128x3 48.1 (no spills), 128x4 44.9, 128x5 43.3,
-// 128x6 41.3 (85 regs, 24 warps/SM), 128x8 43.1.
+// CTA = FWD_THREADS rays = 256 / FWD_THREADS CTAs per 16x16 tile.  The march
+// is latency-bound and tolerates spills: occupancy wins.  Measured on C3
+// (ms/frame, 128-thread CTAs x min blocks/SM): x4 (128 regs) 42.0 (r2 code),
+// x5 (96) 42.0, x6 (80) 39.7, x7 (72) 37.3, x8 (64 regs, 32 warps/SM) 37.2,
+// x9 (56) 37.3, x10 (48) 37.7, x12 (40) 40.5.
 #ifndef GSX_FWD_THREADS
 #define GSX_FWD_THREADS 128
 #endif
 #ifndef GSX_FWD_MINB
-#define GSX_FWD_MINB 6
+#define GSX_FWD_MINB 8
 #endif
 constexpr int FWD_THREADS = GSX_FWD_THREADS;
 constexpr int FWD_PER_TILE = 256 / FWD_THREADS;

@@ -36,8 +36,31 @@ struct PixelGrad {
 // (0-2 mu, 3-6 q, 7-9 s, 10 sigma~, 11-37 SH, 38-58 SG axes, 59-65 SG
 // sharpness, 66-86 SG amplitudes), column = lane; padded to 33 columns so
 // both the column writes and the row sums are bank-conflict free.
+// The 87 rows go through the buffer in two halves -- rows 0-37 (geometry,
+// SH), then rows 38-86 (the lobes) -- so it holds 49 rows (6.3 KB per warp).
 constexpr int RED_ROW = 33;
-constexpr int RED_FLOATS = GSX_NREC * RED_ROW;  // per warp
+constexpr int RED_SPLIT = 38;
+constexpr int RED_FLOATS = (GSX_NREC - RED_SPLIT) * RED_ROW;  // per warp
+
+// warp sum of buffer rows [0, nrows) -> atomics into dst[row0 + row]
+__device__ inline void reduce_rows(const float* __restrict__ red, int nrows,
+                                   float* __restrict__ dst) {
+  __syncwarp();
+  for (int row = threadIdx.x & 31; row < nrows; row += 32) {
+    const float* rp = red + row * RED_ROW;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      s0 += rp[k];
+      s1 += rp[k + 1];
+      s2 += rp[k + 2];
+      s3 += rp[k + 3];
+    }
+    const float sum = (s0 + s1) + (s2 + s3);
+    if (sum != 0.f) atomicAdd(dst + row, sum);
+  }
+  __syncwarp();
+}
 
 // Geometry rows (mu, q, s, sigma~) of one (lane, primitive) from the moments.
 __device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64_t p,
@@ -184,6 +207,9 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
     for (int c = 0; c < 3; ++c) col[(11 + 3 * bsh + c) * RED_ROW] = Y[bsh] * gp[c];
   // spherical-Gaussian lobes, one at a time (rolled: keeps the 14 float4 of
   // lobe data out of registers); the lobe value is recomputed, not kept
+  float* gdst = grad + (int64_t)GSX_NREC * p;
+  reduce_rows(red, RED_SPLIT, gdst);
+  col -= RED_SPLIT * RED_ROW;  // lobe rows 38.. land in buffer rows 0..
   const float4* ap = sv.app + GSX_APP_F4 * p;
   const float* inv_an = (const float*)(sv.gaux + 5 * p + 3);
 #pragma unroll 1
@@ -204,22 +230,7 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
     c[(67 + 2 * l) * RED_ROW] = lb * gp[1];
     c[(68 + 2 * l) * RED_ROW] = lb * gp[2];
   }
-  __syncwarp();
-  float* gdst = grad + (int64_t)GSX_NREC * p;
-  for (int row = lane; row < GSX_NREC; row += 32) {
-    const float* rp = red + row * RED_ROW;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-      s0 += rp[k];
-      s1 += rp[k + 1];
-      s2 += rp[k + 2];
-      s3 += rp[k + 3];
-    }
-    const float sum = (s0 + s1) + (s2 + s3);
-    if (sum != 0.f) atomicAdd(gdst + row, sum);
-  }
-  __syncwarp();
+  reduce_rows(red, GSX_NREC - RED_SPLIT, gdst + RED_SPLIT);
 }
 
 __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
