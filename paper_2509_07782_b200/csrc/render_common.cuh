@@ -95,6 +95,12 @@ __device__ inline void morton_decode8(unsigned t, int& x, int& y) {
   y = ((t >> 1) & 1) | ((t >> 2) & 2) | ((t >> 3) & 4) | ((t >> 4) & 8);
 }
 
+__device__ inline float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ inline float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -210,7 +216,11 @@ __device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t 
   float A = fmaf(ydx, ydx, fmaf(ydy, ydy, ydz * ydz));
   if (!(A > 0.f)) return false;
   float B = fmaf(y0x, ydx, fmaf(y0y, ydy, y0z * ydz));
-  float tc = -B / A;
+  // approximate reciprocal / square root (MUFU, ~1 ulp, no slow-path branch):
+  // a 1-ulp error in tc moves q by ~2 sqrt(A) ulp(tc) ~ 1e-5 at most, far
+  // inside the 1e-4 RGB tolerance, and h only bounds the sample range
+  const float iA = __fdividef(1.0f, A);
+  float tc = -B * iA;
   float ycx = fmaf(tc, ydx, y0x), ycy = fmaf(tc, ydy, y0y), ycz = fmaf(tc, ydz, y0z);
   float qmin = fmaf(ycx, ycx, fmaf(ycy, ycy, ycz * ycz));
   if (qmin > 1.0f) return false;
@@ -221,15 +231,18 @@ __device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t 
   cs.kl2 = g1.w;
   cs.sigma = g0.w;
   cs.lsig = g3.w;
-  cs.h = sqrtf(fmaxf((1.0f - qmin) / A, 0.f));
+  cs.h = sqrt_approx(fmaxf((1.0f - qmin) * iA, 0.f));
   return true;
 }
 
 // conservative sample index range [jlo, jhi] within [0, m-1] that may lie
 // inside the ellipsoid (the q <= 1 test decides exactly).
 __device__ inline bool sample_range(const CandSetup& cs, float dtf, int m, int& jlo, int& jhi) {
-  float lo = (-cs.h - cs.del0) / dtf;
-  float hi = (cs.h - cs.del0) / dtf;
+  // floor/ceil below already leave one sample of slack on each side, which
+  // absorbs the approximate reciprocal
+  const float idt = __fdividef(1.0f, dtf);
+  float lo = (-cs.h - cs.del0) * idt;
+  float hi = (cs.h - cs.del0) * idt;
   if (!(hi >= -1.f) || !(lo <= (float)m)) return false;
   lo = fmaxf(lo, -1.f);
   hi = fminf(hi, (float)m);
