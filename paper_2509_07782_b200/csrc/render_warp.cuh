@@ -79,7 +79,11 @@ struct WarpTrav {
 __device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool want, float lo_t,
                                      float hi_t, float gap, WarpTrav& st, WarpSmem& sm,
                                      int& count, uint32_t& visits) {
-  const int lane = threadIdx.x & 31;
+  // 32-bit shared-window addresses of the list and stack: cheap to keep live
+  // (the generic pointers were rematerialised from %tid per store); every lane
+  // stores the same value, so no lane predicate is needed
+  const unsigned a_list = (unsigned)__cvta_generic_to_shared(sm.list);
+  const unsigned a_stack = (unsigned)__cvta_generic_to_shared(sm.stack);
   while (!st.done && count <= LCAP - 4) {
     ++visits;
     PH_CNT(8, 1)
@@ -116,11 +120,11 @@ __device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool wa
       const int32_t c = ch[k];
       if (!((hits >> k) & 1u) || c == GSX_NONE) continue;
       if (c < 0) {
-        if (lane == 0) sm.list[count] = ~c;
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(a_list + 4u * count), "r"(~c) : "memory");
         ++count;
       } else if (next >= 0) {
         if (st.sp < WSTACK) {
-          if (lane == 0) sm.stack[st.sp] = c;
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(a_stack + 4u * st.sp), "r"(c) : "memory");
           ++st.sp;
         } else {
           st.overflow = true;
