@@ -123,6 +123,8 @@ __global__ void k_single(const float* __restrict__ box32, float4* nodes, int32_t
 }
 
 // ---- 4-wide collapse ----------------------------------------------------------
+// Depth-parity collapse (-DGSX_PARITY_COLLAPSE; measured: C3 35.5 vs 35.0 ms
+// with the greedy collapse below).
 // keep[i] = 1 for binary internal nodes at even depth (root included)
 __global__ void k_keep_flags(const int32_t* __restrict__ parents, int64_t n, uint32_t* keep) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,6 +183,104 @@ __global__ void k_collapse(const float4* __restrict__ nodes, const uint32_t* __r
   o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// ---- SAH-greedy 4-wide collapse (default) ---------------------------------------
+// Top down, one frontier level per launch: a BVH4 node starts from the two
+// children of its binary node and repeatedly opens the child with the largest
+// surface area until it has four (the standard greedy wide-BVH collapse).
+// Compared with the depth-parity collapse it fills nodes (leaf children no
+// longer waste slots) and opens big boxes first, so the packet traversal
+// takes fewer node steps.  Child order inside a node is the binary in-order,
+// so the candidate order is deterministic; BVH4 slot numbers are assigned by
+// atomics (their placement, not the traversal, depends on scheduling).
+struct QItem {
+  int32_t bin;  // binary internal node
+  int32_t out;  // its BVH4 slot
+};
+
+__device__ inline float half_area(const float4& lo, const float4& hi) {
+  const float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_greedy_level(const float4* __restrict__ nodes, const QItem* __restrict__ qin,
+                               const uint32_t* __restrict__ nin_p, QItem* __restrict__ qout,
+                               uint32_t* nout_p, uint32_t* n4_p, float4* __restrict__ nodes4) {
+  const uint32_t nin = *nin_p;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += gridDim.x * blockDim.x) {
+    const QItem it = qin[i];
+    float4 lo[4], hi[4];
+    int32_t ref[4];
+    const float4* nd = nodes + 4 * (int64_t)it.bin;
+    lo[0] = nd[0];
+    hi[0] = nd[1];
+    lo[1] = nd[2];
+    hi[1] = nd[3];
+    ref[0] = __float_as_int(lo[0].w);
+    ref[1] = __float_as_int(hi[0].w);
+    int cnt = ref[1] == GSX_NONE ? 1 : 2;
+    while (cnt < 4) {
+      int best = -1;
+      float ba = -1.f;
+      for (int k = 0; k < cnt; ++k) {
+        if (ref[k] < 0) continue;
+        const float a = half_area(lo[k], hi[k]);
+        if (a > ba) {
+          ba = a;
+          best = k;
+        }
+      }
+      if (best < 0) break;
+      const float4* cd = nodes + 4 * (int64_t)ref[best];
+      const float4 l0 = cd[0], h0 = cd[1], l1 = cd[2], h1 = cd[3];
+      const int32_t c0 = __float_as_int(l0.w), c1 = __float_as_int(h0.w);
+      // replace entry `best` by (c0, c1), keeping the in-order sequence
+      for (int k = cnt; k > best + 1; --k) {
+        lo[k] = lo[k - 1];
+        hi[k] = hi[k - 1];
+        ref[k] = ref[k - 1];
+      }
+      lo[best] = l0;
+      hi[best] = h0;
+      ref[best] = c0;
+      lo[best + 1] = l1;
+      hi[best + 1] = h1;
+      ref[best + 1] = c1;
+      ++cnt;
+    }
+    int32_t ch[4];
+    for (int k = 0; k < 4; ++k) {
+      if (k >= cnt) {
+        ch[k] = GSX_NONE;
+        lo[k] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        hi[k] = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+      } else if (ref[k] < 0) {
+        ch[k] = ref[k];
+      } else {
+        const uint32_t slot = atomicAdd(n4_p, 1u);
+        qout[atomicAdd(nout_p, 1u)] = QItem{ref[k], (int32_t)slot};
+        ch[k] = (int32_t)slot;
+      }
+    }
+    float4* o = nodes4 + 8 * (int64_t)it.out;
+    o[0] = make_float4(lo[0].x, lo[1].x, lo[2].x, lo[3].x);
+    o[1] = make_float4(lo[0].y, lo[1].y, lo[2].y, lo[3].y);
+    o[2] = make_float4(lo[0].z, lo[1].z, lo[2].z, lo[3].z);
+    o[3] = make_float4(hi[0].x, hi[1].x, hi[2].x, hi[3].x);
+    o[4] = make_float4(hi[0].y, hi[1].y, hi[2].y, hi[3].y);
+    o[5] = make_float4(hi[0].z, hi[1].z, hi[2].z, hi[3].z);
+    o[6] = make_float4(__int_as_float(ch[0]), __int_as_float(ch[1]), __int_as_float(ch[2]),
+                       __int_as_float(ch[3]));
+    o[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void k_greedy_init(QItem* q, uint32_t* cnt) {
+  q[0] = QItem{0, 0};
+  cnt[0] = 1;  // frontier A size
+  cnt[1] = 0;  // frontier B size
+  cnt[2] = 1;  // BVH4 slots used (root = 0)
+}
+
 __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* children) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
@@ -198,7 +298,41 @@ __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* 
 extern "C" size_t gsx_bvh_arena_bytes(int64_t n) { return bvh_arena_bytes_impl(n); }
 extern "C" size_t gsx_bvh_workspace_bytes(int64_t n) {
   int64_t m = n > 1 ? n : 1;
-  return 3 * gsx_align256(sizeof(int32_t) * m) + gsx_align256(sizeof(uint32_t) * gsx_scan_ws_elems(m));
+  return 3 * gsx_align256(sizeof(int32_t) * m) +
+         gsx_align256(sizeof(uint32_t) * gsx_scan_ws_elems(m)) +
+         2 * gsx_align256(sizeof(QItem) * m) + 256;
+}
+
+// greedy collapse: level-synchronous frontier, host checks for completion every
+// GREEDY_BATCH levels (BVH4 depth is ~log4 n plus the LBVH's imbalance)
+static int greedy_collapse(const BvhView& bv, int64_t n, char* ws, cudaStream_t s) {
+  constexpr int GREEDY_BATCH = 16;
+  size_t seg = gsx_align256(sizeof(int32_t) * n);
+  char* w = ws + 3 * seg + gsx_align256(sizeof(uint32_t) * gsx_scan_ws_elems(n));
+  QItem* qa = (QItem*)w;
+  QItem* qb = (QItem*)(w + gsx_align256(sizeof(QItem) * n));
+  uint32_t* cnt = (uint32_t*)(w + 2 * gsx_align256(sizeof(QItem) * n));
+  k_greedy_init<<<1, 1, 0, s>>>(qa, cnt);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)(sms * 8);
+  for (int level = 0;; ++level) {
+    const int a = level & 1;
+    QItem* qin = a ? qb : qa;
+    QItem* qout = a ? qa : qb;
+    CUDA_CHECK_RET(cudaMemsetAsync(cnt + (1 - a), 0, sizeof(uint32_t), s));
+    k_greedy_level<<<grid, 256, 0, s>>>(bv.nodes, qin, cnt + a, qout, cnt + (1 - a), cnt + 2,
+                                        bv.nodes4);
+    if ((level + 1) % GREEDY_BATCH == 0) {
+      uint32_t h = 0;
+      CUDA_CHECK_RET(cudaMemcpyAsync(&h, cnt + (1 - a), sizeof h, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK_RET(cudaStreamSynchronize(s));
+      if (h == 0) break;
+      if (level > 4 * 64) return GSX_ERR_STACK;  // cannot happen for a valid tree
+    }
+  }
+  return gsx_check_launch();
 }
 
 extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_codes,
@@ -224,11 +358,18 @@ extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_cod
   k_karras<<<gi, 256, 0, s>>>(sorted_codes, perm, n, bv.nodes, bv.parents);
   k_refit<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sv.box32, n, bv.nodes, bv.parents, flags);
   // 4-wide collapse for the packet traversal
+#ifdef GSX_PARITY_COLLAPSE
   k_keep_flags<<<gi, 256, 0, s>>>(bv.parents, n, keep);
   CUDA_CHECK_RET(cudaMemcpyAsync(idx4, keep, sizeof(uint32_t) * (n - 1), cudaMemcpyDeviceToDevice, s));
   gsx_exclusive_scan_u32(idx4, n - 1, sums, s);
   k_collapse<<<gi, 256, 0, s>>>(bv.nodes, keep, idx4, n, bv.nodes4);
   return gsx_check_launch();
+#else
+  (void)keep;
+  (void)idx4;
+  (void)sums;
+  return greedy_collapse(bv, n, w, s);
+#endif
 }
 
 extern "C" int gsx_bvh_export(const void* bvh_arena, int64_t n, float* boxes, int32_t* children,
