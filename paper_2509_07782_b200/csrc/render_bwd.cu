@@ -34,11 +34,12 @@ struct PixelGrad {
 
 // Gradient rows of one warp's shared reduction buffer: row = record slot
 // (0-2 mu, 3-6 q, 7-9 s, 10 sigma~, 11-37 SH, 38-58 SG axes, 59-65 SG
-// sharpness, 66-86 SG amplitudes), column = lane; padded to 33 columns so
-// both the column writes and the row sums are bank-conflict free.
+// sharpness, 66-86 SG amplitudes), column = lane; rows padded to 36 floats:
+// the column writes hit banks (4 row + lane) mod 32 and the row sums read
+// 16-byte vectors conflict-free per quarter warp.
 // The 87 rows go through the buffer in two halves -- rows 0-37 (geometry,
 // SH), then rows 38-86 (the lobes) -- so it holds 49 rows (6.3 KB per warp).
-constexpr int RED_ROW = 33;
+constexpr int RED_ROW = 36;
 constexpr int RED_SPLIT = 38;
 constexpr int RED_FLOATS = (GSX_NREC - RED_SPLIT) * RED_ROW;  // per warp
 
@@ -47,14 +48,15 @@ __device__ inline void reduce_rows(const float* __restrict__ red, int nrows,
                                    float* __restrict__ dst) {
   __syncwarp();
   for (int row = threadIdx.x & 31; row < nrows; row += 32) {
-    const float* rp = red + row * RED_ROW;
+    const float4* rp = (const float4*)(red + row * RED_ROW);
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 32; k += 4) {
-      s0 += rp[k];
-      s1 += rp[k + 1];
-      s2 += rp[k + 2];
-      s3 += rp[k + 3];
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = rp[k];
+      s0 += v.x;
+      s1 += v.y;
+      s2 += v.z;
+      s3 += v.w;
     }
     const float sum = (s0 + s1) + (s2 + s3);
     if (sum != 0.f) atomicAdd(dst + row, sum);
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
                       int64_t tile_begin, int64_t tile_stride, BwdImages im,
                       const unsigned* __restrict__ skip, float* __restrict__ grad) {
   __shared__ WarpSmem smem[BWD_THREADS / 32];
-  extern __shared__ float red_smem[];  // RED_FLOATS per warp
+  extern __shared__ __align__(16) float red_smem[];  // RED_FLOATS per warp
   if (skip && skip[tile_warp_id(BWD_PER_TILE, BWD_THREADS)]) return;  // warp-uniform
   RayCtx r;
   bool hit;
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     k_render_backward_logged(SceneView sv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
                              int64_t tile_stride, BwdImages im, const char* __restrict__ log,
                              long long nw, float* __restrict__ grad) {
-  extern __shared__ float red_smem[];  // RED_FLOATS per warp
+  extern __shared__ __align__(16) float red_smem[];  // RED_FLOATS per warp
   const long long wid = tile_warp_id(BWDL_PER_TILE, BWDL_THREADS);
   if (!log_complete((void*)log, nw)[wid]) return;  // the replay kernel covers this warp
   const int lane = threadIdx.x & 31;
