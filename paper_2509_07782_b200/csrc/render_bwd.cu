@@ -32,105 +32,145 @@ struct PixelGrad {
   float Ctot[3], Dtot, Tend;
 };
 
-// Gradient rows of one warp's shared reduction buffer: row = record slot
-// (0-2 mu, 3-6 q, 7-9 s, 10 sigma~, 11-37 SH, 38-58 SG axes, 59-65 SG
-// sharpness, 66-86 SG amplitudes), column = lane; rows padded to 36 floats:
-// the column writes hit banks (4 row + lane) mod 32 and the row sums read
-// 16-byte vectors conflict-free per quarter warp.
-// The 87 rows go through the buffer in two halves -- rows 0-37 (geometry,
-// SH), then rows 38-86 (the lobes) -- so it holds 49 rows (6.3 KB per warp).
+// ---------------------------------------------------------------------------
+// Pass-2 reduction.  All 32 lanes hold the same candidate p; per lane and p
+// the values below are formed from the moments and reduced over the warp in
+// a shared buffer (row = value, column = lane; rows padded to 36 floats: the
+// column writes hit banks (4 row + lane) mod 32 and the row sums read 16-byte
+// vectors conflict-free per quarter warp).  Rows, in two halves:
+//   A (37 rows): 0-9 geometry moments, 10-36 SH (b, c) -> record 11 + 3b + c
+//   B (49 rows): lobe l at 7l: raw axis sum (3), sharpness, amplitude (3)
+// Geometry enters only through the moment tensors of the lane offsets
+// v = x0 - mu (x0 = the lane's sample base point) and the direction d:
+//   S0 = m0,  S1 = v m0 + d m1,  S2 = v v^T m0 + (v d^T + d v^T) m1 + d d^T m2
+// (6 unique entries), because with y = M v and u = sqrt(k) y every geometry
+// gradient is linear in them (M = iso_inv, header formulas):
+//   dL/dmu = k M^T M S1,  dL/ds_b = k (M S2 M^T)_bb / s_b (unclamped),
+//   dL/dR[a,b] = -sqrt(k) (M S2)_ba / s_b,  dL/dsigma~ = S0 / sigma~,
+// and the SG axis gradient is (I - n n^T)/|a| applied to sum_lanes f d.
+// Those 31 reduced values go to a per-warp batch; every 32 candidates lane c
+// finishes candidate c (matrix algebra, quaternion chain, projections) and
+// issues its atomics -- the per-lane geometry work of the old formulation
+// (~240 instructions per candidate) becomes ~45 + 1/32 of the finish.
 constexpr int RED_ROW = 36;
-constexpr int RED_SPLIT = 38;
-constexpr int RED_FLOATS = (GSX_NREC - RED_SPLIT) * RED_ROW;  // per warp
+constexpr int RED_ROWS_A = 37;
+constexpr int RED_ROWS_B = 49;
+constexpr int RED_FLOATS = RED_ROWS_B * RED_ROW;  // reduction rows per warp
+constexpr int BAT_ROW = 33;                        // 31 values + candidate id, padded
+constexpr int BAT_FLOATS = 32 * BAT_ROW;
+constexpr int BWD_WARP_FLOATS = RED_FLOATS + BAT_FLOATS;  // shared floats per warp
 
-// warp sum of buffer rows [0, nrows) -> atomics into dst[row0 + row]
-__device__ inline void reduce_rows(const float* __restrict__ red, int nrows,
-                                   float* __restrict__ dst) {
-  __syncwarp();
-  for (int row = threadIdx.x & 31; row < nrows; row += 32) {
-    const float4* rp = (const float4*)(red + row * RED_ROW);
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+struct GradBatch {
+  float* red;  // RED_FLOATS
+  float* bat;  // BAT_FLOATS: bat[c][0..9] geometry, [10..30] raw axes, [31] id
+  int n;       // candidates pending (warp-uniform)
+};
+
+__device__ inline float row_sum(const float* __restrict__ red, int row) {
+  const float4* rp = (const float4*)(red + row * RED_ROW);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 v = rp[k];
-      s0 += v.x;
-      s1 += v.y;
-      s2 += v.z;
-      s3 += v.w;
-    }
-    const float sum = (s0 + s1) + (s2 + s3);
-    if (sum != 0.f) atomicAdd(dst + row, sum);
+  for (int k = 0; k < 8; ++k) {
+    const float4 v = rp[k];
+    s0 += v.x;
+    s1 += v.y;
+    s2 += v.z;
+    s3 += v.w;
   }
-  __syncwarp();
+  return (s0 + s1) + (s2 + s3);
 }
 
-// Geometry rows (mu, q, s, sigma~) of one (lane, primitive) from the moments.
-__device__ inline void geometry_grad(const SceneView& sv, const RayCtx& r, int64_t p,
-                                     const SegBase& b, float m0, float m1, float m2,
-                                     float* __restrict__ col) {
-  const float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
-               g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
-  const float4 a0 = __ldg(sv.gaux + 5 * p), a1 = __ldg(sv.gaux + 5 * p + 1),
-               a2 = __ldg(sv.gaux + 5 * p + 2);
-  const float M[9] = {g1.x, g1.y, g1.z, g2.x, g2.y, g2.z, g3.x, g3.y, g3.z};
-  const float v0[3] = {(b.hi[0] - g0.x) + b.lo[0], (b.hi[1] - g0.y) + b.lo[1],
-                       (b.hi[2] - g0.z) + b.lo[2]};
-  float y0[3], yd[3];
+// Finish the pending candidates: lane c owns candidate c of the batch.
+__device__ inline void grad_batch_flush(const SceneView& sv, GradBatch& gb,
+                                        float* __restrict__ grad) {
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+  if (lane < gb.n) {
+    const float* v = gb.bat + lane * BAT_ROW;
+    const int64_t p = __float_as_int(v[31]);
+    const float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
+                 g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
+    const float4 a0 = __ldg(sv.gaux + 5 * p), a1 = __ldg(sv.gaux + 5 * p + 1),
+                 a2 = __ldg(sv.gaux + 5 * p + 2), a3 = __ldg(sv.gaux + 5 * p + 3),
+                 a4 = __ldg(sv.gaux + 5 * p + 4);
+    (void)g0;
+    const float M[9] = {g1.x, g1.y, g1.z, g2.x, g2.y, g2.z, g3.x, g3.y, g3.z};
+    const float S1[3] = {v[1], v[2], v[3]};
+    // S2 symmetric: (xx, yy, zz, xy, xz, yz)
+    const float S2[9] = {v[4], v[7], v[8], v[7], v[5], v[9], v[8], v[9], v[6]};
+    const float sk = a2.x, k = sk * sk;
+    float* gp = grad + (int64_t)GSX_NREC * p;
+    // mean: k M^T (M S1)
+    float y1[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    y0[a] = fmaf(M[3 * a], v0[0], fmaf(M[3 * a + 1], v0[1], M[3 * a + 2] * v0[2]));
-    yd[a] = fmaf(M[3 * a], r.df[0], fmaf(M[3 * a + 1], r.df[1], M[3 * a + 2] * r.df[2]));
-  }
-  const float sk = a2.x, k = sk * sk;
-  // mean
-  float w3[3];
+    for (int a = 0; a < 3; ++a) y1[a] = fmaf(M[3 * a], S1[0], fmaf(M[3 * a + 1], S1[1], M[3 * a + 2] * S1[2]));
 #pragma unroll
-  for (int a = 0; a < 3; ++a) w3[a] = fmaf(y0[a], m0, yd[a] * m1);
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    col[a * RED_ROW] = k * fmaf(M[a], w3[0], fmaf(M[3 + a], w3[1], M[6 + a] * w3[2]));
-  // scales and rotation (a1.yzw = 1/s, a2.yzw = not-clamped masks)
-  const float is[3] = {a1.y, a1.z, a1.w};
-  const float mask[3] = {a2.y, a2.z, a2.w};
-  float u0[3], ud[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    u0[a] = sk * y0[a];
-    ud[a] = sk * yd[a];
-  }
-#pragma unroll
-  for (int bb = 0; bb < 3; ++bb) {
-    float t = fmaf(u0[bb] * u0[bb], m0, fmaf(2.f * u0[bb] * ud[bb], m1, ud[bb] * ud[bb] * m2));
-    col[(7 + bb) * RED_ROW] = mask[bb] * t * is[bb];
-  }
-  float gR[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
+    for (int a = 0; a < 3; ++a) {
+      const float g = k * fmaf(M[a], y1[0], fmaf(M[3 + a], y1[1], M[6 + a] * y1[2]));
+      if (g != 0.f) atomicAdd(gp + a, g);
+    }
+    // MS = M S2 (row b = M_b S2)
+    float MS[9];
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb)
-      gR[3 * a + bb] = -fmaf(u0[bb] * v0[a], m0,
-                             fmaf(fmaf(u0[bb], r.df[a], ud[bb] * v0[a]), m1,
-                                  ud[bb] * r.df[a] * m2)) * is[bb];
-  // R(q) with q normalized (geometry.py:26-42): dR/dq, then the normalization
-  const float w = a0.x, X = a0.y, Yq = a0.z, Z = a0.w;
-  const float dR[4][9] = {
-      {0.f, -2 * Z, 2 * Yq, 2 * Z, 0.f, -2 * X, -2 * Yq, 2 * X, 0.f},
-      {0.f, 2 * Yq, 2 * Z, 2 * Yq, -4 * X, -2 * w, 2 * Z, 2 * w, -4 * X},
-      {-4 * Yq, 2 * X, 2 * w, 2 * X, 0.f, 2 * Z, -2 * w, 2 * Z, -4 * Yq},
-      {-4 * Z, -2 * w, 2 * X, 2 * w, -4 * Z, 2 * Yq, 2 * X, 2 * Yq, 0.f}};
-  float gq[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float acc = 0.f;
+      for (int a = 0; a < 3; ++a)
+        MS[3 * bb + a] = fmaf(M[3 * bb], S2[a], fmaf(M[3 * bb + 1], S2[3 + a], M[3 * bb + 2] * S2[6 + a]));
+    const float is[3] = {a1.y, a1.z, a1.w};
+    const float mask[3] = {a2.y, a2.z, a2.w};
 #pragma unroll
-    for (int e = 0; e < 9; ++e) acc = fmaf(gR[e], dR[c][e], acc);
-    gq[c] = acc;
+    for (int bb = 0; bb < 3; ++bb) {
+      const float t = fmaf(MS[3 * bb], M[3 * bb], fmaf(MS[3 * bb + 1], M[3 * bb + 1], MS[3 * bb + 2] * M[3 * bb + 2]));
+      const float g = mask[bb] * k * t * is[bb];
+      if (g != 0.f) atomicAdd(gp + 7 + bb, g);
+    }
+    float gR[9];  // gR[3a + b] = -sqrt(k) (M S2)_ba / s_b
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) gR[3 * a + bb] = -sk * MS[3 * bb + a] * is[bb];
+    // R(q) with q normalized (geometry.py:26-42): dR/dq, then the normalization
+    const float w = a0.x, X = a0.y, Yq = a0.z, Z = a0.w;
+    const float dR[4][9] = {
+        {0.f, -2 * Z, 2 * Yq, 2 * Z, 0.f, -2 * X, -2 * Yq, 2 * X, 0.f},
+        {0.f, 2 * Yq, 2 * Z, 2 * Yq, -4 * X, -2 * w, 2 * Z, 2 * w, -4 * X},
+        {-4 * Yq, 2 * X, 2 * w, 2 * X, 0.f, 2 * Z, -2 * w, 2 * Z, -4 * Yq},
+        {-4 * Z, -2 * w, 2 * X, 2 * w, -4 * Z, 2 * Yq, 2 * X, 2 * Yq, 0.f}};
+    float gq[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 9; ++e) acc = fmaf(gR[e], dR[c][e], acc);
+      gq[c] = acc;
+    }
+    const float qv[4] = {w, X, Yq, Z};
+    const float dot = gq[0] * w + gq[1] * X + gq[2] * Yq + gq[3] * Z;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float g = (gq[c] - dot * qv[c]) * a1.x;
+      if (g != 0.f) atomicAdd(gp + 3 + c, g);
+    }
+    const float gs = v[0] * a4.w;  // / sigma~
+    if (gs != 0.f) atomicAdd(gp + 10, gs);
+    // SG axes: d/d(raw axis) of the unit axis n is (I - n n^T) / |a|
+    const float4* ap = sv.app + GSX_APP_F4 * p;
+    const float inv_an[7] = {a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, a4.z};
+#pragma unroll 1
+    for (int l = 0; l < 7; ++l) {
+      const float4 ax = __ldg(ap + 9 + 2 * l);
+      const float r0 = v[10 + 3 * l], r1 = v[11 + 3 * l], r2 = v[12 + 3 * l];
+      const float dd = r0 * ax.x + r1 * ax.y + r2 * ax.z;
+      const float ia = inv_an[l];
+      const float gx = (r0 - dd * ax.x) * ia, gy = (r1 - dd * ax.y) * ia,
+                  gz = (r2 - dd * ax.z) * ia;
+      if (gx != 0.f) atomicAdd(gp + 38 + 3 * l, gx);
+      if (gy != 0.f) atomicAdd(gp + 39 + 3 * l, gy);
+      if (gz != 0.f) atomicAdd(gp + 40 + 3 * l, gz);
+    }
   }
-  const float qv[4] = {w, X, Yq, Z};
-  float dot = gq[0] * w + gq[1] * X + gq[2] * Yq + gq[3] * Z;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) col[(3 + c) * RED_ROW] = (gq[c] - dot * qv[c]) * a1.x;
-  col[10 * RED_ROW] = m0 * __ldg(sv.gaux + 5 * p + 4).w;  // / sigma~
+  __syncwarp();
+  gb.n = 0;
 }
 
 // Replay one composited sample (the forward's RayAccum::add_sample) and form
@@ -157,14 +197,14 @@ __device__ inline void sample_adjoint(RayAccum& acc, const PixelGrad& pg, float 
 }
 
 // pass 2 for one staged candidate (all lanes in lockstep).  Every lane writes
-// its 87 values (zeros when it does not see p) as one column of the warp's
-// buffer `red` as soon as they are formed, then lane L sums rows L, L+32,
-// L+64 and issues one atomic per non-zero row: short live ranges, one copy
-// of the reduction, coalesced atomics.
+// its values (zeros when it does not see p) as one column of the warp's
+// reduction buffer as soon as they are formed; lane L then sums rows L, L+32
+// of each half: direct rows go to atomics, the geometry / axis rows to the
+// batch (see the section comment above).
 __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int64_t p, bool want,
                                       int mc, const SegBase& base, float dtf, const float* Y,
                                       const PixelGrad& pg, const float (&wos)[16],
-                                      const float (&hh)[16], float* __restrict__ red,
+                                      const float (&hh)[16], GradBatch& gb,
                                       float* __restrict__ grad) {
   CandSetup cs;
   int jlo = 0, jhi = -1;
@@ -172,7 +212,7 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
              sample_range(cs, dtf, mc, jlo, jhi);
   if (!__any_sync(FULL, use)) return;
   const int lane = threadIdx.x & 31;
-  float* col = red + lane;
+  float* col = gb.red + lane;
   float pre[3];
   eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, r.df, pre, nullptr);
   const float gcl =
@@ -199,46 +239,78 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
     }
   }
   // lanes that do not see p have zero moments: every value below is 0
-  geometry_grad(sv, r, p, base, m0, m1, m2, col);
-  float gp[3];
+  {
+    const float4 g0 = __ldg(sv.geo + 4 * p);
+    const float v0[3] = {(base.hi[0] - g0.x) + base.lo[0], (base.hi[1] - g0.y) + base.lo[1],
+                         (base.hi[2] - g0.z) + base.lo[2]};
+    const float* d = r.df;
+    col[0] = m0;
 #pragma unroll
-  for (int c = 0; c < 3; ++c) gp[c] = (use && pre[c] > 0.f) ? pg.gC[c] * e0 : 0.f;
+    for (int a = 0; a < 3; ++a) col[(1 + a) * RED_ROW] = fmaf(v0[a], m0, d[a] * m1);
+    // S2 (xx, yy, zz, xy, xz, yz)
+    const int ia[6] = {0, 1, 2, 0, 0, 1}, ib[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const float va = v0[ia[e]], vb = v0[ib[e]], da = d[ia[e]], db = d[ib[e]];
+      col[(4 + e) * RED_ROW] = fmaf(va * vb, m0, fmaf(fmaf(va, db, da * vb), m1, da * db * m2));
+    }
+  }
+  float gpc[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) gpc[c] = (use && pre[c] > 0.f) ? pg.gC[c] * e0 : 0.f;
 #pragma unroll
   for (int bsh = 0; bsh < 9; ++bsh)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) col[(11 + 3 * bsh + c) * RED_ROW] = Y[bsh] * gp[c];
-  // spherical-Gaussian lobes, one at a time (rolled: keeps the 14 float4 of
-  // lobe data out of registers); the lobe value is recomputed, not kept
+    for (int c = 0; c < 3; ++c) col[(10 + 3 * bsh + c) * RED_ROW] = Y[bsh] * gpc[c];
+  // half A: geometry moments -> batch, SH -> atomics
   float* gdst = grad + (int64_t)GSX_NREC * p;
-  reduce_rows(red, RED_SPLIT, gdst);
-  col -= RED_SPLIT * RED_ROW;  // lobe rows 38.. land in buffer rows 0..
+  float* brow = gb.bat + gb.n * BAT_ROW;
+  __syncwarp();
+  for (int row = lane; row < RED_ROWS_A; row += 32) {
+    const float sum = row_sum(gb.red, row);
+    if (row < 10)
+      brow[row] = sum;
+    else if (sum != 0.f)
+      atomicAdd(gdst + 11 + (row - 10), sum);
+  }
+  if (lane == 0) brow[31] = __int_as_float((int)p);
+  __syncwarp();
+  // half B: spherical-Gaussian lobes, one at a time (rolled: keeps the 14
+  // float4 of lobe data out of registers); the lobe value is recomputed
   const float4* ap = sv.app + GSX_APP_F4 * p;
-  const float* inv_an = (const float*)(sv.gaux + 5 * p + 3);
 #pragma unroll 1
   for (int l = 0; l < 7; ++l) {
     const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
     const float cs2 = fmaf(ax.x, r.df[0], fmaf(ax.y, r.df[1], ax.z * r.df[2]));
     const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
-    const float ga = am.x * gp[0] + am.y * gp[1] + am.z * gp[2];
-    float* c = col + l * RED_ROW;
-    c[59 * RED_ROW] = lb * (cs2 - 1.f) * ga;
+    const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
     const float f = lb * ax.w * ga;
-    // d/d(raw axis) of the unit axis: (I - n n^T) / |a| applied to f d
-    const float dd = f * cs2, ia = __ldg(inv_an + l);
-    c[(38 + 2 * l) * RED_ROW] = fmaf(f, r.df[0], -dd * ax.x) * ia;
-    c[(39 + 2 * l) * RED_ROW] = fmaf(f, r.df[1], -dd * ax.y) * ia;
-    c[(40 + 2 * l) * RED_ROW] = fmaf(f, r.df[2], -dd * ax.z) * ia;
-    c[(66 + 2 * l) * RED_ROW] = lb * gp[0];
-    c[(67 + 2 * l) * RED_ROW] = lb * gp[1];
-    c[(68 + 2 * l) * RED_ROW] = lb * gp[2];
+    float* c = col + 7 * l * RED_ROW;
+    c[0] = f * r.df[0];
+    c[RED_ROW] = f * r.df[1];
+    c[2 * RED_ROW] = f * r.df[2];
+    c[3 * RED_ROW] = lb * (cs2 - 1.f) * ga;
+    c[4 * RED_ROW] = lb * gpc[0];
+    c[5 * RED_ROW] = lb * gpc[1];
+    c[6 * RED_ROW] = lb * gpc[2];
   }
-  reduce_rows(red, GSX_NREC - RED_SPLIT, gdst + RED_SPLIT);
+  __syncwarp();
+  for (int row = lane; row < RED_ROWS_B; row += 32) {
+    const float sum = row_sum(gb.red, row);
+    const int l = row / 7, k = row - 7 * l;
+    if (k < 3)
+      brow[10 + 3 * l + k] = sum;
+    else if (sum != 0.f)
+      atomicAdd(gdst + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)), sum);
+  }
+  __syncwarp();
+  if (++gb.n == 32) grad_batch_flush(sv, gb, grad);
 }
 
 __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                  bool want, const Seg& seg, int ns, const float* Y,
                                  RayAccum& acc, const PixelGrad& pg, Counters<false>& cnt,
-                                 WarpSmem& sm, float* __restrict__ red, float* __restrict__ grad) {
+                                 WarpSmem& sm, GradBatch& gb, float* __restrict__ grad) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
   const int nchunks = (ns + 15) / 16;
@@ -307,7 +379,7 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
     for (;;) {
       if (!st2.done) warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st2, sm, count, v2);
       for (int i = 0; i < count; ++i)
-        grad_candidate(sv, r, (int64_t)sm.list[i], want, mc, base, dtf, Y, pg, wos, hh, red,
+        grad_candidate(sv, r, (int64_t)sm.list[i], want, mc, base, dtf, Y, pg, wos, hh, gb,
                        grad);
       __syncwarp();
       if (st2.done) break;
@@ -381,7 +453,7 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
                       int64_t tile_begin, int64_t tile_stride, BwdImages im,
                       const unsigned* __restrict__ skip, float* __restrict__ grad) {
   __shared__ WarpSmem smem[BWD_THREADS / 32];
-  extern __shared__ __align__(16) float red_smem[];  // RED_FLOATS per warp
+  extern __shared__ __align__(16) float red_smem[];  // BWD_WARP_FLOATS per warp
   if (skip && skip[tile_warp_id(BWD_PER_TILE, BWD_THREADS)]) return;  // warp-uniform
   RayCtx r;
   bool hit;
@@ -396,10 +468,12 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
   Counters<false> cnt;
   const int ns = (int)cfg.n_s;
   WarpSmem& sm = smem[threadIdx.x >> 5];
+  float* wsm = red_smem + (threadIdx.x >> 5) * BWD_WARP_FLOATS;
+  GradBatch gb{wsm, wsm + RED_FLOATS, 0};
   march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, [&](const Seg& seg, bool want) {
-    return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm,
-                            red_smem + (threadIdx.x >> 5) * RED_FLOATS, grad);
+    return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm, gb, grad);
   });
+  grad_batch_flush(sv, gb, grad);
 }
 
 // Logged backward: walks the warp's march-log chain (march_log.cuh).  Per
@@ -419,7 +493,7 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     k_render_backward_logged(SceneView sv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
                              int64_t tile_stride, BwdImages im, const char* __restrict__ log,
                              long long nw, float* __restrict__ grad) {
-  extern __shared__ __align__(16) float red_smem[];  // RED_FLOATS per warp
+  extern __shared__ __align__(16) float red_smem[];  // BWD_WARP_FLOATS per warp
   const long long wid = tile_warp_id(BWDL_PER_TILE, BWDL_THREADS);
   if (!log_complete((void*)log, nw)[wid]) return;  // the replay kernel covers this warp
   const int lane = threadIdx.x & 31;
@@ -433,7 +507,8 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
   acc.init();
   float Y[9];
   sh_basis_f(r.df, Y);
-  float* red = red_smem + (threadIdx.x >> 5) * RED_FLOATS;
+  float* wsm = red_smem + (threadIdx.x >> 5) * BWD_WARP_FLOATS;
+  GradBatch gb{wsm, wsm + RED_FLOATS, 0};
   long long off = log_first((void*)log)[wid];
   while (off >= 0) {
     const long long start = off;
@@ -482,19 +557,20 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
         const int nb = min(32, count - i0);
         for (int k = 0; k < nb; ++k)
           grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), want, mc, base, dtf, Y, pg,
-                         wos, hh, red, grad);
+                         wos, hh, gb, grad);
       }
       if (o == off) break;
       o = ho->next;
     }
     off = next;
   }
+  grad_batch_flush(sv, gb, grad);
 }
 
 }  // namespace
 
-constexpr int BWD_SMEM = (BWD_THREADS / 32) * RED_FLOATS * (int)sizeof(float);
-constexpr int BWDL_SMEM = (BWDL_THREADS / 32) * RED_FLOATS * (int)sizeof(float);
+constexpr int BWD_SMEM = (BWD_THREADS / 32) * BWD_WARP_FLOATS * (int)sizeof(float);
+constexpr int BWDL_SMEM = (BWDL_THREADS / 32) * BWD_WARP_FLOATS * (int)sizeof(float);
 
 static int bwd_smem_setup() {
   static bool done = false;  // idempotent; the attribute is per function
