@@ -249,6 +249,22 @@ int gsx_adam_step(float* params, const float* grad, float* m, float* v, int64_t 
                   const float* lr87, const float* lo87, double beta1, double beta2, double eps,
                   int64_t step, void* stream);
 
+/* ---- densification statistics (densify.py:49-83, observe_scene :190-204) ----
+ * Observe one camera from the analytic gradient grad [n,87] (after the
+ * multi-GPU all-reduce): for each observed primitive i (indices[0..m) or all
+ * n when indices is NULL) sum_raw[i] += |dL/dmu_i|, sum_weighted[i] +=
+ * alpha_i |dL/dmu_i| with alpha_i = |mu_i - center| / focal, counts[i] += 1
+ * (float64 / int64 device arrays, GradAccumulator.observe semantics;
+ * center is a host double[3]).  criteria: crit_* [n] u8 = counts >= 1 and
+ * mean > tau (criterion_old: raw, criterion_new: weighted; either may be
+ * NULL). */
+int gsx_densify_observe(const float* grad, const float* params, int64_t n, const int64_t* indices,
+                        int64_t m, const double* center, double focal, double* sum_raw,
+                        double* sum_weighted, int64_t* counts, void* stream);
+int gsx_densify_criteria(const double* sum_raw, const double* sum_weighted, const int64_t* counts,
+                         int64_t n, double tau, uint8_t* crit_old, uint8_t* crit_new,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -99,7 +99,7 @@ class Trainer:
 
     def __init__(self, scene, camera: Camera, cfg: RenderConfig | None = None,
                  loss_cfg: LossConfig = LossConfig(), iso_cfg: IsoLossConfig = IsoLossConfig(),
-                 lr=None, group=None, march_log: bool = True):
+                 lr=None, group=None, march_log: bool = True, densify=None):
         import torch.distributed as dist
 
         self.scene, self.camera = scene, camera
@@ -124,6 +124,8 @@ class Trainer:
         self.log = (MarchLog(camera, tile_begin=self.rank, tile_stride=self.world, device=dev)
                     if march_log else None)
         self._steps = 0
+        # optional densify.GradAccumulator observing every step's view
+        self.densify = densify
 
     def step(self, target, want_loss: bool = False):
         """One optimization step against `target` [H,W,3] (CUDA).  Returns the
@@ -149,6 +151,8 @@ class Trainer:
                                  float(self.iso_cfg.lambda_s), ptr(self.grad), ptr(self._iso),
                                  stream_ptr()), "iso_loss")
         allreduce_grad(self.grad, self.group)
+        if self.densify is not None:  # |dL/dmu| of this view, before the update
+            self.densify.observe_view(self.grad, s.params, self.camera)
         self.adam.step(self.grad)
         self._steps += 1
         if self.log is not None and (self._steps == 1 or want_loss):
