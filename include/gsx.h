@@ -261,6 +261,11 @@ int gsx_adam_step(float* params, const float* grad, float* m, float* v, int64_t 
 int gsx_densify_observe(const float* grad, const float* params, int64_t n, const int64_t* indices,
                         int64_t m, const double* center, double focal, double* sum_raw,
                         double* sum_weighted, int64_t* counts, void* stream);
+/* neighbor_density (densify.py:86-97): counts[i] = number of OTHER means
+ * within the closed ball |mu_j - mu_i| <= radius (fp64 distances of the f32
+ * means, exact BVH pruning), int64 [n] device. */
+int gsx_neighbor_density(const void* scene_arena, const void* bvh_arena, int64_t n, double radius,
+                         int64_t* counts, gsx_dev_status* dev_status, void* stream);
 int gsx_densify_criteria(const double* sum_raw, const double* sum_weighted, const int64_t* counts,
                          int64_t n, double tau, uint8_t* crit_old, uint8_t* crit_new,
                          void* stream);

@@ -7,7 +7,7 @@ kernels (libgsx.so, C ABI in include/gsx.h).  There is no CPU fallback.
 
 from .config import Camera, Ray, RenderConfig, RenderStats, quat_to_rotation, segment_step
 from .densify import (DensifyConfig, GradAccumulator, criterion_new, criterion_old,
-                      observe_scene)
+                      neighbor_density, observe_scene)
 from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptyScene, GsrayError,
                      ParseError, ValidationError)
 from .renderer import (MarchLog, clip_ray_to_scene, march_ray, march_rays, psnr, render,
@@ -30,7 +30,7 @@ def look_at_camera(center, target, focal, width, height, up=(0.0, 1.0, 0.0), **k
 
 __all__ = [
     "BufferOverflow", "Camera", "DegenerateCenter", "DensifyConfig", "GradAccumulator",
-    "MarchLog", "criterion_new", "criterion_old", "observe_scene", "EmptyIsosurface", "EmptyScene",
+    "MarchLog", "criterion_new", "criterion_old", "neighbor_density", "observe_scene", "EmptyIsosurface", "EmptyScene",
     "GsrayError", "ParseError", "Ray", "RenderConfig", "RenderStats", "Scene",
     "ValidationError", "clip_ray_to_scene", "gen_test_scene", "load_scene", "look_at_camera",
     "march_ray", "march_rays", "orbit_cameras", "psnr", "quat_to_rotation", "render",

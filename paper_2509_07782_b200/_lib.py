@@ -104,6 +104,7 @@ _SIGS = {
                                          P, P]),
     "gsx_march_log_usage": (INT, [P, P, P, P]),
     "gsx_densify_observe": (INT, [P, P, I64, P, I64, P, D, P, P, P, P]),
+    "gsx_neighbor_density": (INT, [P, P, I64, D, P, P, P]),
     "gsx_densify_criteria": (INT, [P, P, P, I64, D, P, P, P]),
     "gsx_calibrate_fp32": (INT, [I64, P, P, P]),
     "gsx_image_loss_workspace_bytes": (SZ, [I64, I64, I64]),

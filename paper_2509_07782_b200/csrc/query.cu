@@ -145,6 +145,55 @@ __global__ void k_closest(SceneView sv, BvhView bv, int64_t n, const double* __r
   t_out[qi] = isfinite(best) ? best : NAN;
 }
 
+// neighbor_density (densify.py:86-97): for each primitive, the number of
+// OTHER means within the closed ball of radius r (cKDTree.query_ball_point
+// minus self).  One thread per primitive over the binary BVH: the fp32
+// outward-rounded node boxes contain every mean below them, so pruning on the
+// point-to-box distance is exact; leaves compare fp64 squared distances.
+__global__ void k_neighbors(SceneView sv, BvhView bv, int64_t n, double r2, int64_t* counts,
+                            gsx_dev_status* st) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 gi = __ldg(sv.geo + 4 * i);
+  const double p[3] = {gi.x, gi.y, gi.z};
+  int32_t stack[GSX_STACK];
+  int sp = 0;
+  stack[sp++] = 0;
+  int64_t count = 0;
+  while (sp > 0) {
+    const float4* nd = bv.nodes + 4 * (int64_t)stack[--sp];
+    const float4 a = nd[0], b = nd[1], c = nd[2], e = nd[3];
+    const int32_t ch[2] = {__float_as_int(a.w), __float_as_int(b.w)};
+    const float4 los[2] = {a, c}, his[2] = {b, e};
+    for (int k = 0; k < 2; ++k) {
+      const int32_t c2 = ch[k];
+      if (c2 == GSX_NONE) continue;
+      if (c2 < 0) {
+        const int64_t j = ~(int64_t)c2;
+        if (j == i) continue;
+        const float4 gj = __ldg(sv.geo + 4 * j);
+        const double dx = (double)gj.x - p[0], dy = (double)gj.y - p[1], dz = (double)gj.z - p[2];
+        if (dx * dx + dy * dy + dz * dz <= r2) ++count;
+      } else {
+        const double lo[3] = {los[k].x, los[k].y, los[k].z}, hi[3] = {his[k].x, his[k].y, his[k].z};
+        double d2 = 0.0;
+        for (int ax = 0; ax < 3; ++ax) {
+          const double t = p[ax] < lo[ax] ? lo[ax] - p[ax] : (p[ax] > hi[ax] ? p[ax] - hi[ax] : 0.0);
+          d2 += t * t;
+        }
+        if (d2 > r2) continue;
+        if (sp >= GSX_STACK) {
+          dev_fail(st, GSX_ERR_STACK, i);
+          counts[i] = -1;
+          return;
+        }
+        stack[sp++] = c2;
+      }
+    }
+  }
+  counts[i] = count;
+}
+
 }  // namespace
 
 extern "C" int gsx_collect_segments(const void* scene_arena, const void* bvh_arena, int64_t n,
@@ -167,5 +216,17 @@ extern "C" int gsx_closest_hit(const void* scene_arena, const void* bvh_arena, i
   BvhView bv = bvh_view((void*)bvh_arena, n);
   k_closest<<<(unsigned)((m + 127) / 128), 128, 0, (cudaStream_t)stream>>>(sv, bv, n, queries, m,
                                                                            t_out);
+  return gsx_check_launch();
+}
+
+extern "C" int gsx_neighbor_density(const void* scene_arena, const void* bvh_arena, int64_t n,
+                                    double radius, int64_t* counts, gsx_dev_status* dev_status,
+                                    void* stream) {
+  if (n <= 0) return GSX_ERR_EMPTY;
+  if (!(radius > 0.0) || !counts) return GSX_ERR_ARG;
+  SceneView sv = scene_view((void*)scene_arena, n);
+  BvhView bv = bvh_view((void*)bvh_arena, n);
+  k_neighbors<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      sv, bv, n, radius * radius, counts, dev_status);
   return gsx_check_launch();
 }

@@ -118,6 +118,44 @@ def criterion_new(acc: GradAccumulator, cfg: DensifyConfig):
     return _criterion(acc, cfg, weighted=True)
 
 
+def _point_records(pts):
+    """Degenerate primitives at the given points (s = S_MIN, unit sigma~): the
+    BVH over their boxes is a BVH over the points."""
+    import numpy as np
+
+    rec = np.zeros((len(pts), 87), dtype=np.float32)
+    rec[:, 0:3] = pts
+    rec[:, 3] = 1.0
+    rec[:, 7:10] = 1e-7
+    rec[:, 10] = 1.0
+    rec[:, 40::3][:, :7] = 1.0  # SG axes (0, 0, 1): valid, never evaluated
+    return rec
+
+
+def neighbor_density(means, radius: float):
+    """Number of other points within the closed ball of the given radius
+    (densify.py:86-97, cKDTree.query_ball_point minus self), on the GPU over
+    the scene BVH (`gsx_neighbor_density`).  `means` is a Scene (uses its
+    means and BVH; returns an int64 device tensor in storage order) or an
+    [N,3] array (rounded to float32 like a .gsx record; returns numpy)."""
+    import numpy as np
+
+    from .scene import Scene
+
+    if radius <= 0:
+        raise ValueError("radius must be positive")
+    as_numpy = not isinstance(means, Scene)
+    scene = means if not as_numpy else Scene.from_records(
+        _point_records(np.asarray(means, dtype=float).reshape(-1, 3)))
+    L = _lib.lib()
+    counts = torch.empty(scene.n, dtype=torch.int64, device=scene.device)
+    st = _lib.new_status(scene.device)
+    check(L.gsx_neighbor_density(ptr(scene.arena), ptr(scene.bvh_arena), scene.n, float(radius),
+                                 ptr(counts), ptr(st), stream_ptr()), "neighbor_density")
+    _lib.raise_status(st, "neighbor_density")
+    return counts.cpu().numpy() if as_numpy else counts
+
+
 def observe_scene(acc: GradAccumulator, scene, camera, target, indices=None,
                   loss_cfg: LossConfig | None = None, render_cfg=None):
     """Record one camera observation (densify.py:190-204): render, image loss,

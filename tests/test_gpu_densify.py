@@ -114,3 +114,34 @@ def test_trainer_observes_every_step():
     torch.cuda.synchronize()
     assert acc.counts.cpu().numpy().tolist() == [3] * 50
     assert float(acc.sum_raw.sum()) > 0.0
+
+
+def test_neighbor_density_matches_reference_cases():
+    """densify.py:86-97; the reference's own test_densify.py cases."""
+    import paper_2509_07782_b200 as G
+
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-1, 1, size=(300, 3)).astype(np.float32).astype(np.float64)
+    r = 0.3
+    d = np.linalg.norm(pts[:, None, :] - pts[None, :, :], axis=2)
+    np.testing.assert_array_equal(G.neighbor_density(pts, r), (d <= r).sum(axis=1) - 1)
+    pts = np.array([[0.0, 0, 0], [1.0, 0, 0], [2.5, 0, 0]])
+    assert list(G.neighbor_density(pts, 1.0)) == [1, 1, 0]
+    with pytest.raises(ValueError):
+        G.neighbor_density(np.zeros((2, 3)), 0.0)
+
+
+def test_neighbor_density_scene_vs_ckdtree():
+    from scipy.spatial import cKDTree
+
+    import paper_2509_07782_b200 as G
+    from paper_2509_07782_b200.scenes import f32_records, gen_test_scene_records
+
+    rec = f32_records(gen_test_scene_records("random-cloud", 20_000, seed=2, base_scale=0.02))
+    scene = G.Scene.from_records(rec)
+    G.reorder_by_morton(scene)
+    means = scene.records()[:, 0:3]
+    tree = cKDTree(means)
+    want = np.array([len(ix) - 1 for ix in tree.query_ball_point(means, r=0.125)])
+    got = G.neighbor_density(scene, 0.125).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
