@@ -107,3 +107,26 @@ def test_tiny_dt_dense_sampling():
     rec = f32_records(gen_test_scene_records("random-cloud", count=20, seed=1, anisotropy=2.0))
     cam = G.orbit_cameras(1, radius=3.0, focal=24.0, width=8, height=8)[0]
     _cmp_camera(rec, cam, dict(dt=0.0005, t_eps=1e-8))
+
+
+def test_load_ply_scene_on_device(tmp_path):
+    """PLY -> [N,87] records -> device scene (gsx_prepare validation, BVH) ->
+    render, against the oracle on the same records (tests/golden/io.npz)."""
+    from conftest import golden
+
+    import oracle as O
+    import paper_2509_07782_b200 as G
+
+    g = golden("io")
+    p = tmp_path / "cloud.ply"
+    p.write_bytes(g["ply_binary"].tobytes())
+    scene = G.load_ply_scene(p)
+    assert scene.n == 300
+    np.testing.assert_array_equal(scene.records().astype(np.float32), g["records_binary"])
+    cam = G.orbit_cameras(1, radius=6.0, focal=24.0, width=16, height=16)[0]
+    cfg = G.RenderConfig(mode="adaptive")
+    rgb = G.render(scene, cam, cfg)[0].cpu().numpy()
+    osc = O.OracleScene(g["records_binary"].astype(np.float64))
+    R = osc.render(O.camera_rays(cam.center, cam.quat, cam.focal, 16, 16), 16, 16,
+                   O.OCfg.make(mode="adaptive"))[0]
+    assert np.abs(rgb - R.reshape(16, 16, 3)).max() < 1e-4
