@@ -191,6 +191,15 @@ int gsx_render_rays(const void* scene_arena, const void* bvh_arena, int64_t n,
                     float* rgb, float* depth, float* trans, gsx_stats* stats,
                     gsx_dev_status* dev_status, void* stream);
 
+/* Per-ray RenderStats: per_ray [m,10] u64 = (ray?, samples, segments,
+ * segments_skipped, closest_hit_calls, node_visits, aabb_hits, ellipsoid_hits,
+ * pairs, composited) of each ray (bench.false_positive_fraction
+ * bench.py:181-198 needs them per ray); outputs as gsx_render_rays. */
+int gsx_render_rays_stats(const void* scene_arena, const void* bvh_arena, int64_t n,
+                          const double* rays, int64_t m, int clip, const gsx_render_cfg* cfg,
+                          float* rgb, float* depth, float* trans, uint64_t* per_ray,
+                          gsx_dev_status* dev_status, void* stream);
+
 /* ---- backward (no reference counterpart: SURVEY.md Appendix C) -------------
  * Replays the forward march of the same tiles, and accumulates (atomically,
  * with warp-shuffle pre-reduction) dL/dparams into grad [n,87] f32 in record

@@ -94,10 +94,17 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
 }
 
 template <bool STATS>
-__device__ void flush_stats(gsx_stats* st, const Counters<STATS>& c, bool is_ray) {
-  if (!STATS || !st) return;
+__device__ void flush_stats(gsx_stats* st, const Counters<STATS>& c, bool is_ray,
+                            unsigned long long* per_ray = nullptr) {
+  if (!STATS) return;
   uint32_t v[10] = {is_ray ? 1u : 0u, c.samples, c.segments, c.skipped, c.ch_calls, c.visits,
                     c.aabb, c.ell, c.pairs, c.composited};
+  if (per_ray) {  // one row of 10 counters per ray, no reduction
+    if (is_ray)
+      for (int k = 0; k < 10; ++k) per_ray[k] = v[k];
+    return;
+  }
+  if (!st) return;
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
     uint32_t x = v[k];
@@ -168,7 +175,8 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv
                                                         const double* __restrict__ rays,
                                                         int64_t m, int clip, gsx_render_cfg cfg,
                                                         float* rgb, float* depth, float* trans,
-                                                        gsx_stats* stats) {
+                                                        gsx_stats* stats,
+                                                        unsigned long long* per_ray) {
   __shared__ WarpSmem smem[8];
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = i < m;
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv
     if (depth) depth[i] = acc.D;
     if (trans) trans[i] = T;
   }
-  flush_stats<STATS>(stats, cnt, valid);
+  flush_stats<STATS>(stats, cnt, valid, per_ray ? per_ray + 10 * i : nullptr);
 }
 
 __global__ void k_ffma(int64_t iters, float* sink) {
@@ -331,9 +339,28 @@ extern "C" int gsx_render_rays(const void* scene_arena, const void* bvh_arena, i
   unsigned blocks = (unsigned)((m + 255) / 256);
   if (stats)
     k_render_rays<true><<<blocks, 256, 0, s>>>(sv, bv, rays, m, clip, *cfg, rgb, depth, trans,
-                                               stats);
+                                               stats, nullptr);
   else
     k_render_rays<false><<<blocks, 256, 0, s>>>(sv, bv, rays, m, clip, *cfg, rgb, depth, trans,
-                                                nullptr);
+                                                nullptr, nullptr);
+  return gsx_check_launch();
+}
+
+extern "C" int gsx_render_rays_stats(const void* scene_arena, const void* bvh_arena, int64_t n,
+                                     const double* rays, int64_t m, int clip,
+                                     const gsx_render_cfg* cfg, float* rgb, float* depth,
+                                     float* trans, uint64_t* per_ray,
+                                     gsx_dev_status* dev_status, void* stream) {
+  int rc = gsx_validate_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return GSX_ERR_EMPTY;
+  if (!per_ray) return GSX_ERR_ARG;
+  if (m <= 0) return GSX_OK;
+  SceneView sv = scene_view((void*)scene_arena, n);
+  BvhView bv = bvh_view((void*)bvh_arena, n);
+  (void)dev_status;
+  k_render_rays<true><<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      sv, bv, rays, m, clip, *cfg, rgb, depth, trans, nullptr,
+      (unsigned long long*)per_ray);
   return gsx_check_launch();
 }

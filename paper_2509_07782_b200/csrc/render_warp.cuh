@@ -190,6 +190,11 @@ __device__ inline void for_each_chunk(const BvhView& bv, const RayCtx& r, bool w
 struct Seg {
   double t0, t1, tbase, dt, ds;
   int m;
+  // sample j sits at tgrid + (j0 + j + 0.5) dt, exactly as the reference
+  // forms it (uniform: global grid from t_n; adaptive: from t_s)
+  double tgrid;
+  long long j0;
+  long long cap;  // buffer_capacity (stats only: reference overflow splitting)
 };
 
 struct SegLimits {
@@ -306,18 +311,55 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
   PH_BEGIN(ph_ph)
   if (STATS) {
     if (want) {
-      uint32_t before = cnt.aabb;
-      uint32_t v2 = 0;
-      auto count_fn = [&](int64_t p) -> bool {
-        if (exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) {
-          nonempty = true;
-          cnt.aabb++;
-          if (ellipsoid_hits_interval(sv, r, p, seg.t0, seg.t1)) cnt.ell++;
-        }
-        return false;
+      // exact reference counts: AABB overlaps (with inverted "phantom"
+      // intervals) and ellipsoid hits of [a, b]
+      auto count = [&](double a, double b, uint32_t& na, uint32_t& ne) {
+        na = ne = 0;
+        uint32_t v2 = 0;
+        auto fn = [&](int64_t p) -> bool {
+          if (exact_aabb_overlap(sv, r, p, a, b)) {
+            na++;
+            if (ellipsoid_hits_interval(sv, r, p, a, b)) ne++;
+          }
+          return false;
+        };
+        traverse_segment<true>(bv, r, (float)a, (float)b, fn, v2);
       };
-      traverse_segment<true>(bv, r, (float)seg.t0, (float)seg.t1, count_fn, v2);
-      cnt.pairs += (uint32_t)seg.m * (cnt.aabb - before);
+      // _collect_split (renderer.py:361-393): a collect of more than
+      // buffer_capacity boxes splits the segment at its midpoint (samples
+      // t_j < mid go left) until it fits or holds one sample; every leaf
+      // collect that is non-empty counts one segment, its samples and its
+      // hits -- the reference's counters, not just its image
+      struct Part {
+        double a, b;
+        int jlo, jhi;
+      };
+      Part stk[12];
+      int sp = 0;
+      stk[sp++] = Part{seg.t0, seg.t1, 0, seg.m};
+      bool any = false;
+      while (sp > 0) {
+        const Part q = stk[--sp];
+        uint32_t na, ne;
+        count(q.a, q.b, na, ne);
+        if (na == 0) continue;
+        const int ns = q.jhi - q.jlo;
+        if ((int64_t)na <= seg.cap || ns <= 1 || sp + 2 > 12) {
+          any = true;
+          cnt.segments++;
+          cnt.samples += (uint32_t)ns;
+          cnt.aabb += na;
+          cnt.ell += ne;
+          cnt.pairs += (uint32_t)ns * na;
+          continue;
+        }
+        const double mid = 0.5 * (q.a + q.b);
+        int js = q.jlo;
+        while (js < q.jhi && seg.tgrid + ((double)(seg.j0 + js) + 0.5) * seg.dt < mid) ++js;
+        stk[sp++] = Part{mid, q.b, js, q.jhi};  // right popped after left
+        stk[sp++] = Part{q.a, mid, q.jlo, js};
+      }
+      nonempty = any;
     }
   } else if (want && !nonempty) {
     // no true overlap: empty unless an inverted-interval ("phantom") overlap exists
@@ -381,7 +423,7 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
       else
         active = t_s < t_f && acc.transmittance() > cfg.t_eps;
     }
-    Seg seg{0, 0, 0, 0, 0, 0};
+    Seg seg{0, 0, 0, 0, 0, 0, 0.0, 0, cfg.buffer_capacity};
     if (active) {
       if (uniform) {
         seg.t0 = t_n + (double)k * ds_u;
@@ -392,6 +434,8 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
         for (int j = 0; j < ns; ++j)
           if (t_n + ((double)(j0 + j) + 0.5) * cfg.dt < t_f) seg.m = j + 1;
         seg.tbase = t_n + ((double)j0 + 0.5) * cfg.dt;
+        seg.tgrid = t_n;
+        seg.j0 = j0;
       } else {
         seg.ds = segment_step(cfg, t_s, (double)acc.transmittance());
         seg.dt = seg.ds / (double)ns;
@@ -401,6 +445,8 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
         for (int j = 0; j < ns; ++j)
           if (t_s + ((double)j + 0.5) * seg.dt < t_f) seg.m = j + 1;
         seg.tbase = t_s + 0.5 * seg.dt;
+        seg.tgrid = t_s;
+        seg.j0 = 0;
       }
     }
     if (!__any_sync(FULL, active)) break;
@@ -423,11 +469,7 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
     const bool ne = segfn(seg, go);
     PH_BEGIN(ph_adv)
     if (go) {
-      if (ne) {
-        if (STATS) {
-          cnt.segments++;
-          cnt.samples += seg.m;
-        }
+      if (ne) {  // (STATS: segments / samples are counted by emptiness_tail)
         if (uniform)
           k += 1;
         else

@@ -181,6 +181,26 @@ def march_rays(scene, rays, cfg: RenderConfig, clip: bool = False, stats: bool =
             trans.cpu().numpy().astype(np.float64), s)
 
 
+def ray_stats(scene, rays, cfg: RenderConfig, clip: bool = False):
+    """Per-ray RenderStats counters of a batch of explicit rays [M,8]:
+    int64 numpy [M,10] (rays, samples, segments, segments_skipped,
+    closest_hit_calls, node_visits, aabb_hits, ellipsoid_hits, pairs,
+    composited), march_ray semantics unless clip (gsx_render_rays_stats)."""
+    import ctypes
+
+    L = _lib.lib()
+    dev = scene.device
+    r = torch.as_tensor(np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 8), device=dev)
+    m = r.shape[0]
+    rgb = torch.empty((m, 3), dtype=torch.float32, device=dev)
+    per = torch.zeros((m, 10), dtype=torch.int64, device=dev)
+    cfg_c = cfg.to_c()
+    check(L.gsx_render_rays_stats(ptr(scene.arena), ptr(scene.bvh_arena), scene.n, ptr(r), m,
+                                  int(bool(clip)), ctypes.byref(cfg_c), ptr(rgb), None, None,
+                                  ptr(per), None, stream_ptr()), "render_rays_stats")
+    return per.cpu().numpy()
+
+
 def march_ray(scene, ray: Ray, cfg: RenderConfig, stats: RenderStats | None = None):
     """renderer.py:263-285: (rgb (3,), stats) with stats.transmittance set."""
     if stats is None:

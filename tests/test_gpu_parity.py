@@ -266,9 +266,10 @@ def test_render_small_vs_reference(G, scene, cname):
     ref = g[f"{scene}.{cname}.stats"]
     got = [stats.rays, stats.samples, stats.segments, stats.segments_skipped,
            stats.closest_hit_calls]
-    if cname != "uniform_bg_cap2":  # the reference counts overflow sub-segments
-        assert got == list(ref[:5])
-        assert stats.aabb_hits == ref[6] and stats.ellipsoid_hits == ref[7]
+    # including buffer_capacity=2, where the reference splits overflowing
+    # collects and counts every sub-collect (_collect_split renderer.py:361-393)
+    assert got == list(ref[:5])
+    assert stats.aabb_hits == ref[6] and stats.ellipsoid_hits == ref[7]
 
 
 def test_render_camera_b(G):
