@@ -118,6 +118,25 @@ class Camera:
         d = d / np.linalg.norm(d)
         return Ray(self.center, d, self.t_near, self.t_far)
 
+    def rays(self, pixels=None) -> np.ndarray:
+        """[M,8] float64 (o, d, t_near, t_far) of the given (px, py) pixels
+        (all pixels, row-major, when None) -- Camera.ray vectorised."""
+        if pixels is None:
+            py, px = np.mgrid[0:self.height, 0:self.width]
+            pixels = np.stack([px.ravel(), py.ravel()], axis=1)
+        pix = np.asarray(pixels, dtype=np.float64).reshape(-1, 2)
+        d_cam = np.stack([(pix[:, 0] + 0.5 - 0.5 * self.width) / self.focal,
+                          (pix[:, 1] + 0.5 - 0.5 * self.height) / self.focal,
+                          np.ones(len(pix))], axis=1)
+        d = d_cam @ self.rotation.T
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        out = np.empty((len(pix), 8))
+        out[:, 0:3] = self.center
+        out[:, 3:6] = d
+        out[:, 6] = self.t_near
+        out[:, 7] = self.t_far
+        return out
+
     def to_c(self) -> CameraC:
         c = CameraC()
         R = np.ascontiguousarray(self.rotation, dtype=np.float64).ravel()

@@ -78,3 +78,17 @@ def test_product_package_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(_lib.GsxUnavailable):
         G.Scene.from_records([[0.0] * 87])
+
+
+def test_camera_rays_vectorised_matches_ray():
+    import numpy as np
+
+    import paper_2509_07782_b200 as G
+
+    cam = G.orbit_cameras(2, radius=3.5, focal=40.0, width=9, height=7)[1]
+    r = cam.rays()
+    assert r.shape == (63, 8)
+    for py, px in ((0, 0), (3, 5), (6, 8)):
+        one = cam.ray(px, py)
+        np.testing.assert_array_equal(r[py * 9 + px, 0:3], one.origin)
+        np.testing.assert_allclose(r[py * 9 + px, 3:6], one.direction, rtol=0, atol=1e-15)
