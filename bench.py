@@ -66,17 +66,25 @@ def workload(name: str):
         desc = ("C2 NeRF-synthetic-shaped: 300k Gaussians on/under a sphere of radius 1.5, "
                 "800x800, f=1111.1, white background, uniform dt=0.0025 + ESS")
         return rec, 0.01, cam, dict(mode="uniform", background=(1.0, 1.0, 1.0)), desc
+    if name == "c4":
+        rec = synth_records("ball", 3_000_000, seed=0, anisotropy=3.0, r_max_bound=10.0,
+                            shell_fraction=0.3, shell_radius=(10.0, 50.0))
+        cam = dict(radius=3.5, focal=1.2 * 1237, width=1237, height=822)
+        desc = ("C4 3M Gaussians (C3 generator: 70% ball + 30% background shell), "
+                "1237x822, adaptive+ESS, full train step")
+        return rec, 0.01, cam, dict(mode="adaptive"), desc
     raise ValueError(name)
 
 
-def train_step_bench(G, dev, steps: int, warmup: int):
-    """C2 training step (fwd + L1/DSSIM loss + bwd + iso loss + Adam, BVH rebuilt
-    every step) on one GPU; target = render of the scene with jittered means."""
+def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2"):
+    """Training step (fwd + L1/DSSIM loss + bwd + iso loss + Adam, BVH rebuilt
+    every step) on one GPU; target = render of the scene with jittered means.
+    C2 by default; C4 (3M, 1237x822) with --train-config c4."""
     import torch
 
     from paper_2509_07782_b200.train import Trainer
 
-    rec, eps, cam_kw, cfg_kw, desc = workload("c2")
+    rec, eps, cam_kw, cfg_kw, desc = workload(config)
     cam = make_camera(G, cam_kw)
     cfg = G.RenderConfig(**cfg_kw)
     tscene = G.Scene.from_records(rec)
@@ -263,6 +271,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-config", default="c2", choices=["c2", "c4"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -443,7 +452,8 @@ def main():
     if not args.no_train and world == 1:
         del scene
         torch.cuda.empty_cache()
-        out["train_step"] = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3)
+        out["train_step"] = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3,
+                                             config=args.train_config)
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
