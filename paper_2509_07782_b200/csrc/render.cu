@@ -120,7 +120,7 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
   float Y[9];
   sh_basis_f(r.df, Y);
   const int ns = (int)cfg.n_s;
-  march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_FWD, [&](const Seg& seg, bool want) {
+  march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_FWD, sm, [&](const Seg& seg, bool want) {
     return forward_segment<STATS, SAVE>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm, lw);
   });
 }

@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
   WarpSmem& sm = smem[threadIdx.x >> 5];
   float* wsm = red_smem + (threadIdx.x >> 5) * BWD_WARP_FLOATS;
   GradBatch gb{wsm, wsm + RED_FLOATS, 0};
-  march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, [&](const Seg& seg, bool want) {
+  march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, sm, [&](const Seg& seg, bool want) {
     return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm, gb, grad);
   });
   grad_batch_flush(sv, gb, grad);

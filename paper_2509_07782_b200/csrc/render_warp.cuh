@@ -186,6 +186,103 @@ __device__ inline void for_each_chunk(const BvhView& bv, const RayCtx& r, bool w
   }
 }
 
+// Warp-cooperative ESS closest hit (closest_hit spatial.py:309-354): the
+// lanes with `want` find their first ellipsoid entry in [t_lo, t_hi].  One
+// packet traversal of the 4-wide BVH serves all of them (node loads and loop
+// control shared, no per-lane stacks in local memory): a child is entered
+// when any requesting lane's ray meets its box within [t_lo, min(t_hi, best)]
+// (true intersection, fp32 with margin); children are visited near-first by
+// the lowest requesting lane's entry distance so `best` shrinks early.  Leaf
+// tests are the per-lane fp64 ones of closest_hit_r, and the result -- the
+// minimum entry over every ellipsoid meeting [t_lo, t_hi] -- does not depend
+// on the visiting order, so it equals the per-lane traversal's bit for bit.
+__device__ inline bool warp_closest_hit(const SceneView& sv, const BvhView& bv, const RayCtx& r,
+                                        bool want, double t_lo, double t_hi, double& hit,
+                                        WarpSmem& sm, uint32_t& visits) {
+  want = want && !(t_lo > t_hi);
+  const unsigned req = __ballot_sync(FULL, want);
+  if (!req) return false;
+  const int leader = __ffs(req) - 1;
+  double best = INFINITY;
+  const float lo_t = (float)t_lo - margin(r, (float)t_lo);
+  const unsigned a_stack = (unsigned)__cvta_generic_to_shared(sm.stack);
+  int sp = 0;
+  int32_t node = 0;
+  for (;;) {
+    ++visits;
+    const float4* nd = bv.nodes4 + 8 * (int64_t)node;
+    const float4 lx = __ldg(nd), ly = __ldg(nd + 1), lz = __ldg(nd + 2);
+    const float4 hx = __ldg(nd + 3), hy = __ldg(nd + 4), hz = __ldg(nd + 5);
+    const float4 cf = __ldg(nd + 6);
+    const float clo[3][4] = {{lx.x, lx.y, lx.z, lx.w}, {ly.x, ly.y, ly.z, ly.w},
+                             {lz.x, lz.y, lz.z, lz.w}};
+    const float chi[3][4] = {{hx.x, hx.y, hx.z, hx.w}, {hy.x, hy.y, hy.z, hy.w},
+                             {hz.x, hz.y, hz.z, hz.w}};
+    const int32_t ch[4] = {__float_as_int(cf.x), __float_as_int(cf.y), __float_as_int(cf.z),
+                           __float_as_int(cf.w)};
+    const double lim = t_hi < best ? t_hi : best;
+    const float limf = (float)lim + margin(r, (float)lim);
+    bool hk[4];
+    float ent[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float x0 = (clo[0][k] - r.of[0]) * r.invf[0], x1 = (chi[0][k] - r.of[0]) * r.invf[0];
+      float y0 = (clo[1][k] - r.of[1]) * r.invf[1], y1 = (chi[1][k] - r.of[1]) * r.invf[1];
+      float z0 = (clo[2][k] - r.of[2]) * r.invf[2], z1 = (chi[2][k] - r.of[2]) * r.invf[2];
+      float mn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+      float mx = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+      hk[k] = want && ch[k] != GSX_NONE && mn <= limf && mx >= lo_t && mn <= mx + margin(r, mx);
+      ent[k] = __shfl_sync(FULL, hk[k] ? mn : INFINITY, leader);
+    }
+    // near-first order by the leader's entry (4-element sorting network)
+    int ord[4] = {0, 1, 2, 3};
+#define GSX_CSWAP(i, j) \
+    if (ent[ord[j]] < ent[ord[i]]) { const int t_ = ord[i]; ord[i] = ord[j]; ord[j] = t_; }
+    GSX_CSWAP(0, 1) GSX_CSWAP(2, 3) GSX_CSWAP(0, 2) GSX_CSWAP(1, 3) GSX_CSWAP(1, 2)
+#undef GSX_CSWAP
+    int32_t next = -1;
+    // leaves first (in near order): they can only shrink `best`
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = ord[i];
+      const bool h = hk[k];
+      if (!__any_sync(FULL, h) || ch[k] >= 0) continue;
+      if (h) {
+        const int64_t p = ~(int64_t)ch[k];
+        double y0[3], yd[3];
+        local_frame(sv.geo, p, r, y0, yd);
+        double tin, tout;
+        const double l2 = t_hi < best ? t_hi : best;
+        if (ray_ellipsoid_interval64(y0, yd, t_lo, l2, tin, tout) && tin < best) best = tin;
+      }
+    }
+    // inner children: descend into the nearest, push the others far-first
+#pragma unroll
+    for (int i = 3; i >= 0; --i) {
+      const int k = ord[i];
+      if (!__any_sync(FULL, hk[k]) || ch[k] < 0) continue;
+      if (next >= 0 && sp < WSTACK) {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(a_stack + 4u * sp), "r"(next) : "memory");
+        ++sp;
+      }
+      next = ch[k];
+    }
+    __syncwarp();
+    if (next < 0) {
+      if (sp == 0) break;
+      --sp;
+      next = sm.stack[sp];
+    }
+    node = next;
+  }
+  __syncwarp();
+  if (want && best < INFINITY) {
+    hit = best;
+    return true;
+  }
+  return false;
+}
+
 // per-lane description of the segment processed in this warp iteration
 struct Seg {
   double t0, t1, tbase, dt, ds;
@@ -381,7 +478,8 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
 template <bool STATS, class SegFn>
 __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                   bool hit, const gsx_render_cfg& cfg, const RayAccum& acc,
-                                  Counters<STATS>& cnt, float sync, SegFn&& segfn) {
+                                  Counters<STATS>& cnt, float sync, WarpSmem& sm,
+                                  SegFn&& segfn) {
   const int ns = (int)cfg.n_s;
   const bool uniform = cfg.mode == 0;
   const double t_n = r.t_n, t_f = r.t_f;
@@ -402,19 +500,22 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
   double ch_from = t_n;
   while (__any_sync(FULL, active)) {
     PH_BEGIN(ph_ch)
-    if (need_ch) {
-      double h;
-      if (STATS) cnt.ch_calls++;
-      if (!closest_hit_r(sv, bv, r, ch_from, t_f, h, visits)) {
-        active = false;
-      } else if (uniform) {
-        const long long kk = (long long)((h - t_n) / ds_u), kmin = first_ch ? 0 : k + 1;
-        k = kk > kmin ? kk : kmin;
-      } else {
-        t_s = h;  // adaptive mode has no global grid: restart here
+    if (__any_sync(FULL, need_ch)) {
+      double h = 0.0;
+      const bool got = warp_closest_hit(sv, bv, r, need_ch, ch_from, t_f, h, sm, visits);
+      if (need_ch) {
+        if (STATS) cnt.ch_calls++;
+        if (!got) {
+          active = false;
+        } else if (uniform) {
+          const long long kk = (long long)((h - t_n) / ds_u), kmin = first_ch ? 0 : k + 1;
+          k = kk > kmin ? kk : kmin;
+        } else {
+          t_s = h;  // adaptive mode has no global grid: restart here
+        }
+        need_ch = false;
+        first_ch = false;
       }
-      need_ch = false;
-      first_ch = false;
     }
     PH_END(0, ph_ch)
     if (active) {
