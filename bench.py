@@ -438,7 +438,10 @@ def main():
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "peak_source": "measured FFMA loop (gsx_calibrate_fp32) in this run",
             "flops_per_frame": flops_frame,
-            "flops_model": "33*pairs + 15*samples + 165*ellipsoid_hits + 12*node_visits (SURVEY 8(d))"}
+            "flops_model": ("33*pairs + 15*samples + 165*ellipsoid_hits + 12*node_visits "
+                            "(SURVEY 8(d)); pairs = samples x AABB overlaps per Alg. 1 "
+                            "segment; samples / ellipsoid_hits in the reference's RenderStats "
+                            "semantics (incl. its buffer-overflow sub-collects)")}
     out = {
         "metric": METRIC, "value": mrays, "unit": "Mrays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "fps": 1e3 / ms,

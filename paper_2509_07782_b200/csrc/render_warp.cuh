@@ -434,11 +434,15 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
       Part stk[12];
       int sp = 0;
       stk[sp++] = Part{seg.t0, seg.t1, 0, seg.m};
-      bool any = false;
+      bool any = false, top = true;
       while (sp > 0) {
         const Part q = stk[--sp];
         uint32_t na, ne;
         count(q.a, q.b, na, ne);
+        // `pairs` (ours, the roofline's work unit) is per Alg. 1 segment:
+        // samples x AABB overlaps of the whole segment, as the kernel does it
+        if (top) cnt.pairs += (uint32_t)seg.m * na;
+        top = false;
         if (na == 0) continue;
         const int ns = q.jhi - q.jlo;
         if ((int64_t)na <= seg.cap || ns <= 1 || sp + 2 > 12) {
@@ -447,7 +451,6 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
           cnt.samples += (uint32_t)ns;
           cnt.aabb += na;
           cnt.ell += ne;
-          cnt.pairs += (uint32_t)ns * na;
           continue;
         }
         const double mid = 0.5 * (q.a + q.b);
