@@ -157,6 +157,10 @@ int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_codes, const i
                   int64_t n, void* bvh_arena, void* workspace, void* stream);
 /* export for tests: node child boxes f32 [n-1, 2, 2, 3], children i32 [n-1, 2]
  * (>= 0 internal node, < 0 leaf ~prim), parent i32 [2n-1]. */
+/* Rebuild the 4-wide nodes of bvh_arena from its binary nodes (for a binary
+ * tree written by another builder: root = node 0, children in .w, leaves
+ * ~index); workspace as for gsx_bvh_build. */
+int gsx_bvh_collapse(void* bvh_arena, int64_t n, void* workspace, void* stream);
 int gsx_bvh_export(const void* bvh_arena, int64_t n, float* boxes, int32_t* children,
                    int32_t* parents, void* stream);
 

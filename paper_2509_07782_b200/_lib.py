@@ -93,6 +93,7 @@ _SIGS = {
     "gsx_bvh_workspace_bytes": (SZ, [I64]),
     "gsx_bvh_build": (INT, [P, P, P, I64, P, P, P]),
     "gsx_bvh_export": (INT, [P, I64, P, P, P, P]),
+    "gsx_bvh_collapse": (INT, [P, I64, P, P]),
     "gsx_collect_segments": (INT, [P, P, I64, P, I64, I64, P, P, P, P]),
     "gsx_closest_hit": (INT, [P, P, I64, P, I64, P, P]),
     "gsx_render_forward": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, P, P]),

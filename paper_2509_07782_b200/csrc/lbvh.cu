@@ -372,6 +372,15 @@ extern "C" int gsx_bvh_build(const void* scene_arena, const uint64_t* sorted_cod
 #endif
 }
 
+// Re-derive the 4-wide nodes from the binary nodes already in the arena (after
+// an external builder wrote them, e.g. the SAH experiment in
+// profiles/experiments/).
+extern "C" int gsx_bvh_collapse(void* bvh_arena, int64_t n, void* workspace, void* stream) {
+  if (n <= 1) return n == 1 ? GSX_OK : GSX_ERR_EMPTY;
+  BvhView bv = bvh_view(bvh_arena, n);
+  return greedy_collapse(bv, n, (char*)workspace, (cudaStream_t)stream);
+}
+
 extern "C" int gsx_bvh_export(const void* bvh_arena, int64_t n, float* boxes, int32_t* children,
                               int32_t* parents, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
