@@ -123,14 +123,18 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2"):
     tr.grad.zero_()
     render_backward(scene, cam, cfg, tr.rgb, tr.depth, tr.trans, tr.dI, grad=tr.grad, log=tr.log)
     ev[4].record(s)
-    # for comparison: the replay backward (no march log)
+    # for comparison: the replay backward (no march log) and the plain forward
     tr.grad.zero_()
     render_backward(scene, cam, cfg, tr.rgb, tr.depth, tr.trans, tr.dI, grad=tr.grad)
     ev[5].record(s)
+    ev6 = torch.cuda.Event(enable_timing=True)
+    render(scene, cam, cfg, rgb=tr.rgb, depth=tr.depth, trans=tr.trans)
+    ev6.record(s)
     torch.cuda.synchronize()
     phases = {"rebuild_ms": ev[0].elapsed_time(ev[1]), "forward_ms": ev[1].elapsed_time(ev[2]),
               "loss_ms": ev[2].elapsed_time(ev[3]), "backward_ms": ev[3].elapsed_time(ev[4]),
-              "replay_backward_ms": ev[4].elapsed_time(ev[5])}
+              "replay_backward_ms": ev[4].elapsed_time(ev[5]),
+              "forward_unlogged_ms": ev[5].elapsed_time(ev6)}
     out = {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
            "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
            "rays_per_step": cam_kw["width"] * cam_kw["height"], "phases": phases}
