@@ -17,7 +17,36 @@
 // reference's exact fp64 slab test on the candidates, so ESS jumps and
 // adaptive grid restarts happen exactly where the reference's do.
 // the forward measured faster with the cold paths inlined (C3: 40.3 vs 41.2 ms)
+// Cold fp64 paths (phantom probe, exact AABB test, closest-hit leaf test)
+// inlined: C3 32.9 ms vs 38.2 out of line (cone traversal, no screen).
+#ifndef GSX_COLD
 #define GSX_COLD inline
+#endif
+#ifndef GSX_EXACT_ATTR
+#define GSX_EXACT_ATTR inline
+#endif
+#ifndef GSX_CHLEAF_ATTR
+#define GSX_CHLEAF_ATTR inline
+#endif
+#ifndef GSX_CONE_SCREEN
+#define GSX_CONE_SCREEN 0
+#endif
+#define GSX_SCREEN_SMEM GSX_CONE_SCREEN
+// staged (cp.async double-buffered) candidate data: measured slower (C3
+// 35.5 vs 32.9 ms, C2 19.7 vs 18.3): off
+#ifndef GSX_STAGE_N
+#define GSX_STAGE_N 0
+#endif
+// camera-kernel traversal: 0 per-lane packet (warp_traverse), 1 packet cone
+// (warp_traverse_cone), 2 cone for the plain forward, per-lane packet for the
+// logged (training) forward
+#ifndef GSX_FWD_CONE
+#define GSX_FWD_CONE 1
+#endif
+#ifndef GSX_FWD_CH
+#define GSX_FWD_CH 16
+#endif
+#define FWD_CONE(save) (GSX_FWD_CONE == 1 || (GSX_FWD_CONE == 2 && !(save)))
 #include "gsx_common.cuh"
 #include "march_log.cuh"
 #include "render_warp.cuh"
@@ -30,61 +59,103 @@ using namespace gsx;
 // only help traversing).  Accumulates and composites the lane's samples and
 // returns its exact AABB-emptiness verdict.  SAVE (training) also appends the
 // chunk's candidate stream and per-sample sums to the warp's march log.
-template <bool STATS, bool SAVE>
+template <bool STATS, bool SAVE, bool CONE>
 __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                 bool want, const Seg& seg, int ns, const float* Y,
                                 RayAccum& acc, Counters<STATS>& cnt, WarpSmem& sm,
                                 LogWriter& lw) {
   bool nonempty = false;
   const float dtf = (float)seg.dt;
-  const int nchunks = (ns + 15) / 16;
+  // samples per chunk: the per-sample sums sig[CH], W[CH][3] are the largest
+  // live state of the list loop (CH = 16: 64 registers at a 64-register cap)
+  constexpr int CH = SAVE ? 16 : GSX_FWD_CH;
+  const int nchunks = (ns + CH - 1) / CH;
   uint32_t visits = 0;
   for (int ch = 0; ch < nchunks; ++ch) {
-    int mc = want ? seg.m - ch * 16 : 0;
-    mc = mc < 0 ? 0 : (mc > 16 ? 16 : mc);
-    const double tb = seg.tbase + (double)(ch * 16) * seg.dt;
+    int mc = want ? seg.m - ch * CH : 0;
+    mc = mc < 0 ? 0 : (mc > CH ? CH : mc);
+    // a lane takes part in the chunks that hold its samples (chunk 0 always:
+    // emptiness); the chunks' traversal intervals tile [t0, t1]
+    const bool wch = want && (ch == 0 || mc > 0);
+    const double tb = seg.tbase + (double)(ch * CH) * seg.dt;
     const SegBase base = seg_base(r, tb);
-    float sig[16];
-    float W[16][3];
+    float sig[CH];
+    float W[CH][3];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < CH; ++j) {
       sig[j] = 0.f;
       W[j][0] = W[j][1] = W[j][2] = 0.f;
     }
-    if (!__any_sync(FULL, want && (mc > 0 || ch == 0))) continue;
-    // n_s > 16 processes the segment in 16-sample chunks, each with its own
-    // traversal.  One traversal call site: list chunks of LCAP entries are
-    // traversed, then accumulated, until the stream is exhausted.
-    const SegLimits lim = seg_limits(r, seg);
+    if (!__any_sync(FULL, wch)) continue;
+    // One traversal call site: list chunks of LCAP entries are traversed,
+    // then accumulated, until the stream is exhausted.
+    SegLimits lim;
+    if (nchunks == 1) {
+      lim = seg_limits(r, seg);
+    } else {
+      const double a = ch == 0 ? seg.t0 : seg.tgrid + (double)(seg.j0 + ch * CH) * seg.dt;
+      const double b = (ch + 1) * CH >= seg.m
+                           ? seg.t1
+                           : seg.tgrid + (double)(seg.j0 + (ch + 1) * CH) * seg.dt;
+      lim = interval_limits(r, a, b);
+    }
     WarpTrav st{0, 0, false, false};
+    ConeTrav cst;
+    if (CONE) {
+      make_cone(r, wch, lim.lo_t, lim.hi_t, sm);
+      cone_begin(sm, cst);
+    }
     int count = 0;
     const bool save = SAVE && __any_sync(FULL, want && mc > 0);
-    auto exact = [&](int64_t p) {
-      if (!STATS && want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
+    auto exact = [&](int64_t p, bool gate) {
+      if (!STATS && gate && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
     };
+    bool single = true;
     for (;;) {
       PH_BEGIN(ph_t)
-      warp_traverse(bv, r, want, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
+      if (CONE)
+        warp_traverse_cone(bv, cst, sm, count, visits);
+      else
+        warp_traverse(bv, r, wch, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
       PH_END(1, ph_t)
       PH_BEGIN(ph_p)
-      accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
+#if GSX_CONE_SCREEN
+      if (CONE)
+        accumulate_list_cone(sv, r, sm, count, wch, mc, lim.lo_t, lim.hi_t, base, dtf, Y, sig, W,
+                             exact);
+      else
+#endif
+#if GSX_STAGE_N > 0
+        accumulate_list_staged(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
+#else
+        // the logged forward records only the entries some lane used
+        count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
+#endif
       PH_END(2, ph_p)
-      if (st.done) break;
+      if (CONE ? cst.done : st.done) break;
+      single = false;
       if (save) log_list_chunk(lw, sm.list, count);
       __syncwarp();
       count = 0;
     }
-    if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
+    if (CONE && GSX_CONE_SCREEN && !STATS && single && wch && !nonempty) {
+      // the screen gated the exact test: lanes without a screened overlap
+      // test the whole (single-chunk) list before emptiness_tail's probe
+      for (int i = 0; i < count && !nonempty; ++i) exact(sm.list[i], true);
+    }
+    if constexpr (SAVE) {
+      if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
+    }
     if (STATS) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
+      for (int j = 0; j < CH; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
     }
     PH_BEGIN(ph_c)
     // front-to-back compositing (renderer.py:230-239); zero-density samples
     // leave the state unchanged, so compositing an empty segment is a no-op
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < CH; ++j)
       acc.add_sample(j < mc ? sig[j] : 0.f, W[j], (float)(tb + (double)j * seg.dt), dtf);
     PH_END(3, ph_c)
   }
@@ -113,7 +184,7 @@ __device__ void flush_stats(gsx_stats* st, const Counters<STATS>& c, bool is_ray
   }
 }
 
-template <bool STATS, bool SAVE>
+template <bool STATS, bool SAVE, bool CONE>
 __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayCtx& r, bool hit,
                               const gsx_render_cfg& cfg, RayAccum& acc, Counters<STATS>& cnt,
                               WarpSmem& sm, LogWriter& lw) {
@@ -121,7 +192,7 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
   sh_basis_f(r.df, Y);
   const int ns = (int)cfg.n_s;
   march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_FWD, sm, [&](const Seg& seg, bool want) {
-    return forward_segment<STATS, SAVE>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm, lw);
+    return forward_segment<STATS, SAVE, CONE>(sv, bv, r, want, seg, ns, Y, acc, cnt, sm, lw);
   });
 }
 
@@ -137,28 +208,45 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
 #define GSX_FWD_MINB 8
 #endif
 constexpr int FWD_THREADS = GSX_FWD_THREADS;
-constexpr int FWD_PER_TILE = 256 / FWD_THREADS;
 
+
+// One warp block: the 32 rays of an 8x4 Z-order pixel block.  blk numbers the
+// blocks of the launch: tile tile_begin + (blk / 8) * tile_stride, warp blk % 8
+// of the tile (the march-log warp id).
 template <bool STATS, bool SAVE>
-__global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
-    k_render_camera(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
-                    int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
-                    float* trans, gsx_stats* stats, void* log, long long log_nw) {
-  __shared__ WarpSmem smem[FWD_THREADS / 32];
-  int64_t W = cam.width, H = cam.height;
-  int64_t tiles_x = (W + 15) / 16;
-  int64_t tile = tile_begin + (int64_t)(blockIdx.x / FWD_PER_TILE) * tile_stride;
+__device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
+                                  const gsx_render_cfg& cfg, int64_t tile_begin,
+                                  int64_t tile_stride, long long blk, float* rgb, float* depth,
+                                  float* trans, gsx_stats* stats, void* log, long long log_nw,
+                                  WarpSmem& sw) {
+  const int64_t W = cam.width, H = cam.height;
+  const int64_t tiles_x = (W + 15) / 16;
+  const int64_t tile = tile_begin + (int64_t)(blk >> 3) * tile_stride;
+  const unsigned lane = threadIdx.x & 31;
   int mx, my;
-  morton_decode8((blockIdx.x % FWD_PER_TILE) * FWD_THREADS + threadIdx.x, mx, my);
-  int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
-  bool valid = px < W && py < H;
+  morton_decode8((unsigned)(blk & 7) * 32 + lane, mx, my);
+  const int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
+  const bool valid = px < W && py < H;
   Counters<STATS> cnt;
   RayCtx r;
-  bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
+  const bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
   RayAccum acc;
   acc.init();
-  LogWriter lw = log_writer(SAVE ? log : nullptr, tile_warp_id(FWD_PER_TILE, FWD_THREADS));
-  march_forward<STATS, SAVE>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
+  LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
+#if GSX_CONE_SCREEN
+  {
+    // image-plane coordinates of the lane's pixel and the camera columns for
+    // the silhouette screen (accumulate_list_cone)
+    const float inv_f = (float)(1.0 / cam.focal);
+    sw.uv[lane] = make_float2(((float)px + 0.5f - 0.5f * (float)W) * inv_f,
+                              ((float)py + 0.5f - 0.5f * (float)H) * inv_f);
+    if (lane < 3)
+      sw.camc[lane] =
+          make_float4((float)cam.R[lane], (float)cam.R[3 + lane], (float)cam.R[6 + lane], 0.f);
+    __syncwarp();
+  }
+#endif
+  march_forward<STATS, SAVE, FWD_CONE(SAVE)>(sv, bv, r, hit, cfg, acc, cnt, sw, lw);
   if (SAVE) log_finish(lw, log_nw);
   if (valid) {
     int64_t pix = py * W + px;
@@ -168,6 +256,31 @@ __global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
     if (trans) trans[pix] = T;
   }
   flush_stats<STATS>(stats, cnt, valid);
+}
+
+// (Persistent warps pulling pixel blocks from a launch-wide counter measured
+// slower: C3 34.1 vs 33.9 ms -- the block loop costs registers / spills.)
+template <bool STATS, bool SAVE>
+__global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
+    k_render_camera(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
+                    int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
+                    float* trans, gsx_stats* stats, void* log, long long log_nw) {
+  __shared__ WarpSmem smem[FWD_THREADS / 32];
+  const long long blk = (long long)blockIdx.x * (FWD_THREADS / 32) + (threadIdx.x >> 5);
+  render_warp_block<STATS, SAVE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
+                                 trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
+}
+
+// Launch k_render_camera over ntl tiles (8 warp blocks each).
+template <bool STATS, bool SAVE>
+int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
+                  const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride, int64_t ntl,
+                  float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
+                  long long log_nw, cudaStream_t s) {
+  const long long ctas = 8 * (long long)ntl / (FWD_THREADS / 32);
+  k_render_camera<STATS, SAVE><<<(unsigned)ctas, FWD_THREADS, 0, s>>>(
+      sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, stats, log, log_nw);
+  return gsx_check_launch();
 }
 
 template <bool STATS>
@@ -186,7 +299,7 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv
   RayAccum acc;
   acc.init();
   LogWriter lw = log_writer(nullptr, 0);
-  march_forward<STATS, false>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
+  march_forward<STATS, false, false>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
   if (valid) {
     float T = hit ? acc.transmittance() : 1.f;
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = acc.C[k] + T * (float)cfg.background[k];
@@ -255,18 +368,16 @@ extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena
   if (tile_stride < 1 || tile_begin < 0) return GSX_ERR_ARG;
   int64_t tiles = ((cam->width + 15) / 16) * ((cam->height + 15) / 16);
   if (tile_begin >= tiles) return GSX_OK;
-  int64_t blocks = FWD_PER_TILE * ((tiles - tile_begin + tile_stride - 1) / tile_stride);
+  const int64_t ntl = (tiles - tile_begin + tile_stride - 1) / tile_stride;
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
   cudaStream_t s = (cudaStream_t)stream;
   (void)dev_status;
   if (stats)
-    k_render_camera<true, false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
-        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, stats, nullptr, 0);
-  else
-    k_render_camera<false, false><<<(unsigned)blocks, FWD_THREADS, 0, s>>>(
-        sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr, nullptr, 0);
-  return gsx_check_launch();
+    return launch_camera<true, false>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb,
+                                      depth, trans, stats, nullptr, 0, s);
+  return launch_camera<false, false>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb, depth,
+                                     trans, nullptr, nullptr, 0, s);
 }
 
 __global__ void k_log_init(LogHeader* h, unsigned long long cap, unsigned nw, long long table) {
@@ -307,9 +418,8 @@ extern "C" int gsx_render_forward_logged(const void* scene_arena, const void* bv
   (void)dev_status;
   k_log_init<<<1, 1, 0, s>>>((LogHeader*)log, (unsigned long long)log_bytes,
                              (unsigned)(8 * ntl), table);
-  k_render_camera<false, true><<<(unsigned)(FWD_PER_TILE * ntl), FWD_THREADS, 0, s>>>(
-      sv, bv, *cam, *cfg, tile_begin, tile_stride, rgb, depth, trans, nullptr, log, 8 * ntl);
-  return gsx_check_launch();
+  return launch_camera<false, true>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb, depth,
+                                    trans, nullptr, log, 8 * ntl, s);
 }
 
 extern "C" int gsx_march_log_usage(const void* log, int64_t* used_bytes, int* overflow,

@@ -339,7 +339,7 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
         W[j][0] = W[j][1] = W[j][2] = 0.f;
       }
       // pass 1: the forward's exact accumulation (same candidate order)
-      auto exact = [&](int64_t p) {
+      auto exact = [&](int64_t p, bool) {
         if (want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
       };
       for (;;) {

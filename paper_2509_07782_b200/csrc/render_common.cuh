@@ -8,6 +8,9 @@
 #ifndef GSX_COLD
 #define GSX_COLD __noinline__
 #endif
+#ifndef GSX_FAST_COMPOSITE
+#define GSX_FAST_COMPOSITE 0
+#endif
 
 namespace gsx {
 
@@ -125,22 +128,37 @@ __device__ inline void sh_basis_f(const float* d, float* Y) {
   Y[8] = C2C * (x * x - y * y);
 }
 
+// float4 loaders: read-only global (default) or shared memory (staged copies)
+struct LdgLoad {
+  __device__ float4 operator()(const float4* p) const { return __ldg(p); }
+};
+struct SmemLoad {
+  __device__ float4 operator()(const float4* p) const {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+  }
+};
+
 // unclamped radiance and lobe values (lobes may be NULL); app = GSX_APP_F4
 // float4 in the streaming layout, consumed one float4 at a time so the
 // coefficients never need 76 live registers.
+template <class L = LdgLoad>
 __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const float* Y,
                                          const float* d, float* pre, float* lobes) {
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int b = 0; b < 9; ++b) {
-    const float4 v = __ldg(app + b);
+    const float4 v = L()(app + b);
     s0 = fmaf(Y[b], v.x, s0);
     s1 = fmaf(Y[b], v.y, s1);
     s2 = fmaf(Y[b], v.z, s2);
   }
 #pragma unroll
   for (int l = 0; l < 7; ++l) {
-    const float4 ax = __ldg(app + 9 + 2 * l), am = __ldg(app + 10 + 2 * l);
+    const float4 ax = L()(app + 9 + 2 * l), am = L()(app + 10 + 2 * l);
     float cs = fmaf(ax.x, d[0], fmaf(ax.y, d[1], ax.z * d[2]));
     float e = __expf(ax.w * (cs - 1.0f));
     if (lobes) lobes[l] = e;
@@ -153,10 +171,11 @@ __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const f
   pre[2] = s2;
 }
 
+template <class L = LdgLoad>
 __device__ inline void eval_radiance_f(const float4* __restrict__ app, const float* Y,
                                        const float* d, float* c) {
   float pre[3];
-  eval_radiance_pre(app, Y, d, pre, nullptr);
+  eval_radiance_pre<L>(app, Y, d, pre, nullptr);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) c[ch] = fmaxf(pre[ch], 0.f);
 }
@@ -200,10 +219,10 @@ __device__ inline SegBase seg_base(const RayCtx& r, double tbase) {
 // segment plus a box (~0.3 world units) for any primitive the segment can
 // see -- no catastrophic cancellation, no fp64.  Then y(j) = y0 + (j dt) yd,
 // q(j) = A (j dt - tc)^2 + qmin with qmin = |y0 + tc yd|^2.
-__device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t p,
-                                  const SegBase& b, CandSetup& cs) {
-  float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
-         g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
+template <class L = LdgLoad>
+__device__ inline bool cand_setup_at(const float4* geo, const RayCtx& r, const SegBase& b,
+                                     CandSetup& cs) {
+  const float4 g0 = L()(geo), g1 = L()(geo + 1), g2 = L()(geo + 2), g3 = L()(geo + 3);
   float v0 = (b.hi[0] - g0.x) + b.lo[0];
   float v1 = (b.hi[1] - g0.y) + b.lo[1];
   float v2 = (b.hi[2] - g0.z) + b.lo[2];
@@ -234,6 +253,10 @@ __device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t 
   cs.h = sqrt_approx(fmaxf((1.0f - qmin) * iA, 0.f));
   return true;
 }
+__device__ inline bool cand_setup(const SceneView& sv, const RayCtx& r, int64_t p,
+                                  const SegBase& b, CandSetup& cs) {
+  return cand_setup_at(sv.geo + 4 * p, r, b, cs);
+}
 
 // conservative sample index range [jlo, jhi] within [0, m-1] that may lie
 // inside the ellipsoid (the q <= 1 test decides exactly).
@@ -254,8 +277,11 @@ __device__ inline bool sample_range(const CandSetup& cs, float dtf, int m, int& 
 // ---------------------------------------------------------------------------
 // exact fp64 tests (reference arithmetic) used for ESS emptiness and stats
 // ---------------------------------------------------------------------------
-__device__ inline bool exact_aabb_overlap(const SceneView& sv, const RayCtx& r, int64_t p,
-                                          double t0, double t1) {
+#ifndef GSX_EXACT_ATTR
+#define GSX_EXACT_ATTR inline
+#endif
+__device__ GSX_EXACT_ATTR bool exact_aabb_overlap(const SceneView& sv, const RayCtx& r, int64_t p,
+                                                double t0, double t1) {
   const double* ab = sv.aabb64 + 6 * p;
   double ta, tb;
   box_slab64(ab, ab + 3, r.o, r.d, r.inv_t, ta, tb);
@@ -446,6 +472,31 @@ struct RayAccum {
   __device__ float transmittance() const { return T; }
   // branch-free: a zero-density sample leaves the state unchanged (measured
   // faster than skipping it: C3 40.0 vs 40.5 ms, training forward 24.3 vs 27.0)
+#if GSX_FAST_COMPOSITE
+  // (Off: 0.5 ms faster on C3 but moves C3 pixels by up to 5.8e-5 through
+  // the termination / adaptive-step decisions -- too close to the 1e-4 bar.)
+  // Same arithmetic with MUFU exponentials (16 samples are unrolled per
+  // segment: the libm expm1f / expf bodies cost ~60 instructions of code per
+  // sample).  alpha = 1 - exp(-x): 5-term series below x = 0.05 (truncation
+  // < x^6/720 = 2e-11 relative), else 1 - 2^(-x log2 e) (ex2.approx relative
+  // error ~1e-7, i.e. < 2.4e-6 relative on alpha >= 0.049); T = 2^(-od log2 e)
+  // to ~2e-7 relative.
+  __device__ void add_sample(float sig, const float* W, float tj, float dt) {
+    const bool on = sig > 0.f;
+    const float x = on ? sig * dt : 0.f;
+    const float ser =
+        x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.f / 120.f, -1.f / 24.f), 1.f / 6.f), -0.5f), 1.f);
+    const float big = 1.f - ex2_approx(-1.4426950408889634f * x);
+    const float w = (x < 0.05f ? ser : big) * T;
+    const float s = on ? __fdividef(w, sig) : 0.f;
+    C[0] = fmaf(s, W[0], C[0]);
+    C[1] = fmaf(s, W[1], C[1]);
+    C[2] = fmaf(s, W[2], C[2]);
+    D = fmaf(w, tj, D);
+    od += x;
+    T = ex2_approx(-1.4426950408889634f * od);
+  }
+#else
   __device__ void add_sample(float sig, const float* W, float tj, float dt) {
     const bool on = sig > 0.f;
     const float ods = on ? sig * dt : 0.f;
@@ -458,6 +509,7 @@ struct RayAccum {
     od += ods;
     T = expf(-od);
   }
+#endif
 };
 
 }  // namespace gsx

@@ -25,6 +25,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GSX_SYNC_BWD
 #define GSX_SYNC_BWD 0.5f
 #endif
+#ifndef GSX_SCREEN2
+#define GSX_SCREEN2 1
+#endif
 constexpr int LCAP = 256;    // warp candidate list (shared memory)
 constexpr int WSTACK = 256;  // warp traversal stack (shared memory)
 
@@ -59,9 +62,28 @@ struct Counters {
            pairs = 0, composited = 0;
 };
 
+// Per-warp shared state.  The forward (render.cu) adds the silhouette-screen
+// scratch (GSX_SCREEN_SMEM) and the staged-candidate double buffer
+// (GSX_STAGE_N entries x 27 float4: 4 geo + 23 appearance).
+#ifndef GSX_SCREEN_SMEM
+#define GSX_SCREEN_SMEM 0
+#endif
+#ifndef GSX_STAGE_N
+#define GSX_STAGE_N 0
+#endif
+constexpr int STAGE_F4 = 4 + GSX_APP_F4;
 struct WarpSmem {
   int32_t stack[WSTACK];
   int32_t list[LCAP];
+  float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | 0 | 0)
+#if GSX_SCREEN_SMEM
+  float4 pre[64];   // accumulate_list_cone: per-entry Silhouette (c[32], h[32])
+  float4 camc[3];   // camera columns R_0, R_1, R_2 (fp32; camera kernel only)
+  float2 uv[32];    // lane pixel in image-plane coordinates (camera kernel only)
+#endif
+#if GSX_STAGE_N > 0
+  float4 stage[2][GSX_STAGE_N * STAGE_F4];
+#endif
 };
 
 struct WarpTrav {
@@ -145,6 +167,198 @@ __device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool wa
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Packet-cone traversal (camera rays: one common origin).
+//
+// The lanes that take part in an iteration march rays from one origin o, so
+// their segments lie in the cone {o + t d : d in the lanes' directions} cut by
+// the distance shell |x - o| in [min lo_t, max hi_t] (|d| = 1, so t is the
+// distance).  The cone is bounded by four planes through o: in projective
+// coordinates (u, v) = (d.e1, d.e2) / d.a about the leader's direction a,
+// the lanes span [umin, umax] x [vmin, vmax] and the planes are
+// e1 - umin a, umax a - e1, e2 - vmin a, vmax a - e2 (inward normals).
+// Every box a lane's segment truly meets intersects this region, so the
+// cone's leaf set is a superset of the per-lane union warp_traverse stages
+// (each lane then filters with its own density setup, and the exact fp64
+// emptiness test runs on the list as before).  The test is one box per lane:
+// the 32 lanes test the 4 children of 8 nodes at once -- 8x fewer node steps
+// than the per-lane packet test, where all 32 lanes test the same 4 children.
+// ---------------------------------------------------------------------------
+__device__ inline unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ inline float4 lds4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ inline int32_t lds_i(unsigned a) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ inline void sts_i_if(unsigned a, int32_t v, bool p) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.b32 [%0], %1; }" ::"r"(a),
+               "r"(v), "r"((unsigned)p)
+               : "memory");
+}
+__device__ inline float warp_min(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fminf(x, __shfl_xor_sync(FULL, x, o));
+  return x;
+}
+__device__ inline float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(FULL, x, o));
+  return x;
+}
+
+// Build the cone of the lanes with `want` (at least one) over [lo_t, hi_t]
+// into sm.cone.  Margins: the (u, v) ranges are widened by 2e-5 (the fp32
+// rounding of u, v is ~1e-7), the shell by 1e-6 relative (lo_t / hi_t already
+// carry the traversal margin); boxes are widened in cone_box.
+__device__ inline void make_cone(const RayCtx& r, bool want, float lo_t, float hi_t,
+                                 WarpSmem& sm) {
+  const unsigned m = __ballot_sync(FULL, want);
+  const int leader = __ffs(m) - 1;
+  float a[3], o[3];  // the leader's direction and the (common) origin: lanes
+                    // without a ray (off-image, missing the scene) hold none
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    a[k] = __shfl_sync(FULL, r.df[k], leader);
+    o[k] = __shfl_sync(FULL, r.of[k], leader);
+  }
+  // orthonormal basis around a (Duff et al. 2017, branch-free)
+  const float sg = copysignf(1.f, a[2]);
+  const float ia = -1.f / (sg + a[2]);
+  const float b = a[0] * a[1] * ia;
+  const float e1[3] = {1.f + sg * a[0] * a[0] * ia, sg * b, -sg * a[0]};
+  const float e2[3] = {b, sg + a[1] * a[1] * ia, -a[1]};
+  const float da = r.df[0] * a[0] + r.df[1] * a[1] + r.df[2] * a[2];
+  const float u = (r.df[0] * e1[0] + r.df[1] * e1[1] + r.df[2] * e1[2]) / da;
+  const float v = (r.df[0] * e2[0] + r.df[1] * e2[1] + r.df[2] * e2[2]) / da;
+  const bool bad = __any_sync(FULL, want && !(da > 0.25f));
+  const float umin = warp_min(want ? u : INFINITY) - 2e-5f;
+  const float umax = warp_max(want ? u : -INFINITY) + 2e-5f;
+  const float vmin = warp_min(want ? v : INFINITY) - 2e-5f;
+  const float vmax = warp_max(want ? v : -INFINITY) + 2e-5f;
+  const float tlo = fmaxf(warp_min(want ? lo_t : INFINITY), 0.f) * (1.f - 1e-6f);
+  const float thi = warp_max(want ? hi_t : -INFINITY) * (1.f + 1e-6f);
+  // eps_scale of the taking-part lanes (the others may hold no ray at all)
+  const float es = warp_max(want ? r.eps_scale : 0.f);
+  if ((threadIdx.x & 31) == 0) {
+    // a packet wider than ~75 degrees (never for camera tiles) keeps only the shell
+    float z = bad ? 0.f : 1.f;
+    float th2 = thi * thi, tl2 = tlo * tlo;
+#ifdef GSX_CONE_NOPLANES
+    z = 0.f;
+#endif
+#ifdef GSX_CONE_NOSHELL
+    th2 = INFINITY;
+    tl2 = 0.f;
+#endif
+    sm.cone[0] = make_float4(o[0], o[1], o[2], tl2);
+    sm.cone[1] = make_float4(z * (e1[0] - umin * a[0]), z * (e1[1] - umin * a[1]),
+                             z * (e1[2] - umin * a[2]), th2);
+    sm.cone[2] = make_float4(z * (umax * a[0] - e1[0]), z * (umax * a[1] - e1[1]),
+                             z * (umax * a[2] - e1[2]), es);
+    sm.cone[3] = make_float4(z * (e2[0] - vmin * a[0]), z * (e2[1] - vmin * a[1]),
+                             z * (e2[2] - vmin * a[2]), 0.f);
+    sm.cone[4] = make_float4(z * (vmax * a[0] - e2[0]), z * (vmax * a[1] - e2[1]),
+                             z * (vmax * a[2] - e2[2]), 0.f);
+  }
+  __syncwarp();
+}
+
+// Does box [lo, hi] meet the cone in sm.cone (address a_cone)?  Conservative:
+// the half extents are widened by 1e-6 (|c| + h + eps_scale).
+__device__ inline bool cone_box(unsigned a_cone, float lx, float ly, float lz, float hx,
+                                float hy, float hz) {
+  const float4 c0 = lds4(a_cone);
+  const float es = lds4(a_cone + 32u).w;
+  const float cx = fmaf(0.5f, lx + hx, -c0.x), cy = fmaf(0.5f, ly + hy, -c0.y),
+              cz = fmaf(0.5f, lz + hz, -c0.z);
+  float ex = 0.5f * (hx - lx), ey = 0.5f * (hy - ly), ez = 0.5f * (hz - lz);
+  ex = fmaf(1e-6f, fabsf(cx) + ex + es, ex);
+  ey = fmaf(1e-6f, fabsf(cy) + ey + es, ey);
+  ez = fmaf(1e-6f, fabsf(cz) + ez + es, ez);
+  // distance shell: nearest and farthest box point from o
+  const float nx = fmaxf(fabsf(cx) - ex, 0.f), ny = fmaxf(fabsf(cy) - ey, 0.f),
+              nz = fmaxf(fabsf(cz) - ez, 0.f);
+  const float fx = fabsf(cx) + ex, fy = fabsf(cy) + ey, fz = fabsf(cz) + ez;
+  const float dmin2 = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+  const float dmax2 = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
+  bool ok = dmax2 >= c0.w;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const float4 n = lds4(a_cone + 16u * (1 + p));
+    if (p == 0) ok = ok && dmin2 <= n.w;
+    const float s = fmaf(n.x, cx, fmaf(n.y, cy, fmaf(n.z, cz, fmaf(fabsf(n.x), ex,
+                    fmaf(fabsf(n.y), ey, fabsf(n.z) * ez)))));
+    ok = ok && s >= 0.f;
+  }
+  return ok;
+}
+
+struct ConeTrav {
+  int sp;
+  bool done;
+};
+
+__device__ inline void cone_begin(WarpSmem& sm, ConeTrav& st) {
+  if ((threadIdx.x & 31) == 0) sm.stack[0] = 0;  // root
+  __syncwarp();
+  st.sp = 1;
+  st.done = false;
+}
+
+// Traverse the 4-wide BVH against the cone in sm.cone, appending leaves to
+// sm.list.  Each step pops up to 8 nodes from the shared stack (depth-first:
+// the most recently pushed) and tests their 4 children, one per lane; hit
+// leaves are appended to the list and hit inner children pushed, both in lane
+// order (ballot + popc ranks).  Resumable: returns when the stack is empty
+// (st.done) or the list has fewer than 32 free entries.  The number of nodes
+// popped shrinks as the stack fills (a step pushes at most 3 more than it
+// pops), so the 256-entry stack overflows only for trees deeper than ~80.
+__device__ inline void warp_traverse_cone(const BvhView& bv, ConeTrav& st, WarpSmem& sm,
+                                          int& count, uint32_t& visits) {
+  const unsigned a_list = (unsigned)__cvta_generic_to_shared(sm.list);
+  const unsigned a_stack = (unsigned)__cvta_generic_to_shared(sm.stack);
+  const unsigned a_cone = (unsigned)__cvta_generic_to_shared(sm.cone);
+  const unsigned lane = threadIdx.x & 31, lt = lanemask_lt();
+  const int slot = (int)(lane >> 2), c = (int)(lane & 3);
+  while (st.sp > 0 && count <= LCAP - 32) {
+    int k = st.sp < 8 ? st.sp : 8;
+    const int room = (WSTACK - st.sp) / 3;
+    k = k < room ? k : (room > 1 ? room : 1);
+    const int base = st.sp - k;
+    visits += (uint32_t)k;
+    PH_CNT(8, k)
+    const bool valid = slot < k;
+    const int32_t node = valid ? lds_i(a_stack + 4u * (unsigned)(base + slot)) : 0;
+    const float* nf = (const float*)(bv.nodes4 + 8 * (int64_t)node);
+    const int32_t ch = __float_as_int(__ldg(nf + 24 + c));
+    // (absent children have inf / -inf boxes: NaN centres fail every test)
+    const bool cb = cone_box(a_cone, __ldg(nf + c), __ldg(nf + 4 + c), __ldg(nf + 8 + c),
+                             __ldg(nf + 12 + c), __ldg(nf + 16 + c), __ldg(nf + 20 + c));
+    const bool hit = valid && ch != GSX_NONE && cb;
+    const bool leaf = hit && ch < 0, inner = hit && ch >= 0;
+    const unsigned bl = __ballot_sync(FULL, leaf), bi = __ballot_sync(FULL, inner);
+    sts_i_if(a_list + 4u * (unsigned)(count + __popc(bl & lt)), ~ch, leaf);
+    const int pos = base + __popc(bi & lt);
+    sts_i_if(a_stack + 4u * (unsigned)pos, ch, inner && pos < WSTACK);
+    count += __popc(bl);
+    const int np = base + __popc(bi);
+    st.sp = np < WSTACK ? np : WSTACK;
+    __syncwarp();
+  }
+  st.done = st.sp == 0;
+}
+
 // Visit every candidate of the warp's union traversal: f(p) is called by all
 // 32 lanes in lockstep for each staged primitive p (list chunks of LCAP).
 template <class F>
@@ -196,6 +410,20 @@ __device__ inline void for_each_chunk(const BvhView& bv, const RayCtx& r, bool w
 // tests are the per-lane fp64 ones of closest_hit_r, and the result -- the
 // minimum entry over every ellipsoid meeting [t_lo, t_hi] -- does not depend
 // on the visiting order, so it equals the per-lane traversal's bit for bit.
+// closest-hit leaf test (spatial.py:340-352): min(best, entry) of primitive p
+#ifndef GSX_CHLEAF_ATTR
+#define GSX_CHLEAF_ATTR inline
+#endif
+__device__ GSX_CHLEAF_ATTR double ch_leaf(const SceneView& sv, int64_t p, const RayCtx& r,
+                                          double t_lo, double t_hi, double best) {
+  double y0[3], yd[3];
+  local_frame(sv.geo, p, r, y0, yd);
+  double tin, tout;
+  const double l2 = t_hi < best ? t_hi : best;
+  if (ray_ellipsoid_interval64(y0, yd, t_lo, l2, tin, tout) && tin < best) best = tin;
+  return best;
+}
+
 __device__ inline bool warp_closest_hit(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                         bool want, double t_lo, double t_hi, double& hit,
                                         WarpSmem& sm, uint32_t& visits) {
@@ -247,14 +475,7 @@ __device__ inline bool warp_closest_hit(const SceneView& sv, const BvhView& bv, 
       const int k = ord[i];
       const bool h = hk[k];
       if (!__any_sync(FULL, h) || ch[k] >= 0) continue;
-      if (h) {
-        const int64_t p = ~(int64_t)ch[k];
-        double y0[3], yd[3];
-        local_frame(sv.geo, p, r, y0, yd);
-        double tin, tout;
-        const double l2 = t_hi < best ? t_hi : best;
-        if (ray_ellipsoid_interval64(y0, yd, t_lo, l2, tin, tout) && tin < best) best = tin;
-      }
+      if (h) best = ch_leaf(sv, ~(int64_t)ch[k], r, t_lo, t_hi, best);
     }
     // inner children: descend into the nearest, push the others far-first
 #pragma unroll
@@ -305,6 +526,15 @@ __device__ inline SegLimits seg_limits(const RayCtx& r, const struct Seg& seg) {
   return l;
 }
 
+// traversal limits of an arbitrary interval [a, b] of the ray
+__device__ inline SegLimits interval_limits(const RayCtx& r, double a, double b) {
+  SegLimits l;
+  l.lo_t = (float)a - margin(r, (float)a);
+  l.hi_t = (float)b + margin(r, (float)b);
+  l.gap = margin(r, (float)b);
+  return l;
+}
+
 // Stage the candidates of this iteration's segments: traverse [t0, t1] (with
 // margins).  On return `count` entries are in sm.list; st.done == false means
 // the list is only the first chunk of a longer stream (the caller continues
@@ -329,34 +559,40 @@ struct CandUse {
   int jlo, jhi;
   bool use;
 };
-__device__ inline CandUse candidate_use(const SceneView& sv, const RayCtx& r, int64_t p,
-                                        bool want, int mc, const SegBase& base, float dtf) {
+template <class L = LdgLoad>
+__device__ inline CandUse candidate_use_at(const float4* geo, const RayCtx& r, bool want, int mc,
+                                           const SegBase& base, float dtf) {
   CandUse u;
   u.jlo = 0;
   u.jhi = -1;
-  u.use = want && mc > 0 && cand_setup(sv, r, p, base, u.cs) &&
+  u.use = want && mc > 0 && cand_setup_at<L>(geo, r, base, u.cs) &&
           sample_range(u.cs, dtf, mc, u.jlo, u.jhi);
   return u;
+}
+__device__ inline CandUse candidate_use(const SceneView& sv, const RayCtx& r, int64_t p,
+                                        bool want, int mc, const SegBase& base, float dtf) {
+  return candidate_use_at(sv.geo + 4 * p, r, want, mc, base, dtf);
 }
 
 // Pass-1 accumulation of one candidate into the 16 per-sample sums
 // (renderer.py:218-228), given its setup.
-__device__ inline void accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
-                                       const CandUse& u, float dtf, const float* Y,
-                                       float (&sig)[16], float (&W)[16][3]) {
+template <class L = LdgLoad, int CH = 16>
+__device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, const CandUse& u,
+                                          float dtf, const float* Y, float (&sig)[CH],
+                                          float (&W)[CH][3]) {
   const CandSetup& cs = u.cs;
   const bool use = u.use;
   const int jlo = u.jlo, jhi = u.jhi;
   PH_CNT(9, 1)
   PH_LANES(11, use)
-  if (!__any_sync(FULL, use)) return;
+  if (!__any_sync(FULL, use)) return false;
   PH_CNT(14, 1)
   float c[3] = {0.f, 0.f, 0.f};
-  if (use) eval_radiance_f(sv.app + GSX_APP_F4 * p, Y, r.df, c);
+  if (use) eval_radiance_f<L>(app, Y, r.df, c);
   const float nkl2 = -cs.kl2;
   // 4-sample groups outside every lane's range are skipped warp-uniformly
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 0; g < CH / 4; ++g) {
     if (!__any_sync(FULL, use && jlo <= 4 * g + 3 && jhi >= 4 * g)) continue;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
@@ -373,31 +609,272 @@ __device__ inline void accumulate_used(const SceneView& sv, const RayCtx& r, int
       }
     }
   }
+  return true;
 }
 
-__device__ inline void accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
+template <int CH>
+__device__ inline bool accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
+                                       const CandUse& u, float dtf, const float* Y,
+                                       float (&sig)[CH], float (&W)[CH][3]) {
+  return accumulate_used_at(sv.app + GSX_APP_F4 * p, r, u, dtf, Y, sig, W);
+}
+
+template <int CH>
+__device__ inline bool accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
                                             bool want, int mc, const SegBase& base, float dtf,
-                                            const float* Y, float (&sig)[16],
-                                            float (&W)[16][3]) {
+                                            const float* Y, float (&sig)[CH],
+                                            float (&W)[CH][3]) {
   const CandUse u = candidate_use(sv, r, p, want, mc, base, dtf);
-  accumulate_used(sv, r, p, u, dtf, Y, sig, W);
+  return accumulate_used(sv, r, p, u, dtf, Y, sig, W);
 }
 
 // Pass 1 over a staged list in list order.  (Interleaving two candidates'
 // setups for ILP measured slower: the extra live state spills at 128 regs.)
-template <class Pre>
-__device__ inline void accumulate_list(const SceneView& sv, const RayCtx& r, const WarpSmem& sm,
-                                       int count, bool want, int mc, const SegBase& base,
-                                       float dtf, const float* Y, float (&sig)[16],
-                                       float (&W)[16][3], Pre&& pre) {
+// COMPACT: the list is compacted in place to the entries some lane used (the
+// only ones with a non-zero contribution, hence the only ones the logged
+// backward needs); returns the new count.
+template <bool COMPACT = false, class Pre, int CH>
+__device__ inline int accumulate_list(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
+                                      int count, bool want, int mc, const SegBase& base,
+                                      float dtf, const float* Y, float (&sig)[CH],
+                                      float (&W)[CH][3], Pre&& pre) {
   // (L1 prefetch of the listed geometry / appearance blocks measured slower:
   // 40.9 vs 40.0 ms on C3 -- the entry loop is not load-latency bound)
+  int kept = 0;
   for (int i = 0; i < count; ++i) {
     const int64_t p = sm.list[i];
-    pre(p);
-    accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
+    pre(p, want);
+    const bool used = accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
+    if (COMPACT && used) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) sm.list[kept] = (int32_t)p;
+      ++kept;
+    }
+  }
+  if (COMPACT) __syncwarp();
+  return COMPACT ? kept : count;
+}
+
+// Pass 1 over a cone-staged list (camera rays).  The cone list is a loose
+// superset -- most entries meet no lane's segment -- so every entry is first
+// screened per lane by the exact silhouette of its ellipsoid seen from the
+// camera centre, in image-plane coordinates z = (u, v) (the lane's pixel:
+// u = (px + 0.5 - W/2) / f): the line o + s R (u, v, 1) meets the ellipsoid
+// iff (z - z*)^T Hn (z - z*) <= 1.  The 32 entries of a group are prepared
+// entry-parallel (prep_silhouette), then each lane tests its pixel in ~10
+// instructions instead of the ~60 of the full density setup, plus a depth
+// test against the ellipsoid's bounding sphere.  Only passing lanes run the
+// exact setup (candidate_use) and the exact AABB test; entries no lane passes
+// cost nothing else.  The screen is conservative (tolerances well above its
+// fp32 rounding; near or degenerate views pass everything), so the sums are
+// those of the unscreened list.  Lanes the screen leaves without an exact
+// overlap get `fallback` (the unscreened exact test) after the stream.
+//
+// Silhouette (per entry, fp32): y0 = M (o - mu), rho = |y0|, unit-sphere frame
+// of the ellipsoid.  A direction w hits iff (rho^2 - 1) |P w~|^2 <= (y0^ . w~)^2
+// with w~ = M w and P the projector orthogonal to y0.  Expanding about the
+// direction to mu, z_c = (R^T (mu - o)).xy / (R^T (mu - o)).z, where
+// P M R (z_c, 1) = 0 exactly: with N_j = M R_j (camera columns j = 0, 1),
+// alpha_j = y0^ . N_j, A_j = P N_j, alpha_c = -rho / pz and D = z - z_c,
+//   f(D) = D^T H D - 2 alpha_c beta.D - alpha_c^2 <= 0,
+//   H = (rho^2 - 1) [A_i . A_j] - beta beta^T,  beta = (alpha_0, alpha_1),
+// i.e. (D - D*)^T H (D - D*) <= alpha_c^2 (1 + beta^T H^-1 beta) with
+// D* = alpha_c H^-1 beta.  No term cancels beyond O(1) (the expansion point
+// removes the rho^2 cancellation of the textbook discriminant).
+struct Silhouette {
+  float4 c;  // (centre u, centre v, dmin, dmax)
+  float4 h;  // (Hn00, 2 Hn01, Hn11, limit)
+};
+__device__ inline Silhouette prep_silhouette(const SceneView& sv, int64_t p, const float4& o,
+                                             const float4* camc) {
+  const float4 g0 = __ldg(sv.geo + 4 * p), g1 = __ldg(sv.geo + 4 * p + 1),
+               g2 = __ldg(sv.geo + 4 * p + 2), g3 = __ldg(sv.geo + 4 * p + 3);
+  const float px = o.x - g0.x, py = o.y - g0.y, pz = o.z - g0.z;  // o - mu
+  const float dist = sqrtf(fmaf(px, px, fmaf(py, py, pz * pz)));
+  const float n1 = fmaf(g1.x, g1.x, fmaf(g1.y, g1.y, g1.z * g1.z));
+  const float n2 = fmaf(g2.x, g2.x, fmaf(g2.y, g2.y, g2.z * g2.z));
+  const float n3 = fmaf(g3.x, g3.x, fmaf(g3.y, g3.y, g3.z * g3.z));
+  // largest semi-axis + rounding margins -> distance range of the ellipsoid
+  const float rad = fmaf(rsqrtf(fminf(fminf(n1, n2), n3)), 1.0001f,
+                         1e-6f * (dist + fabsf(o.x) + fabsf(o.y) + fabsf(o.z)));
+  Silhouette s;
+  s.c = make_float4(0.f, 0.f, dist - rad, dist + rad);
+  s.h = make_float4(0.f, 0.f, 0.f, 1.f);  // pass-all
+  const float y0x = fmaf(g1.x, px, fmaf(g1.y, py, g1.z * pz));
+  const float y0y = fmaf(g2.x, px, fmaf(g2.y, py, g2.z * pz));
+  const float y0z = fmaf(g3.x, px, fmaf(g3.y, py, g3.z * pz));
+  const float rho2 = fmaf(y0x, y0x, fmaf(y0y, y0y, y0z * y0z));
+  // camera-frame coordinates of mu - o
+  const float4 R0 = camc[0], R1 = camc[1], R2 = camc[2];
+  const float qx = -fmaf(R0.x, px, fmaf(R0.y, py, R0.z * pz));
+  const float qy = -fmaf(R1.x, px, fmaf(R1.y, py, R1.z * pz));
+  const float qz = -fmaf(R2.x, px, fmaf(R2.y, py, R2.z * pz));
+  // near / inside the ellipsoid, beside or behind the image plane, or so far
+  // that fp32 cannot resolve the silhouette: no screening
+  if (!(rho2 > 1.02f && rho2 < 1e9f && qz > 1e-3f * dist)) return s;
+  const float irho = rsqrtf(rho2);
+  const float ux = y0x * irho, uy = y0y * irho, uz = y0z * irho;
+  // N_j = M R_j
+  const float a0x = fmaf(g1.x, R0.x, fmaf(g1.y, R0.y, g1.z * R0.z));
+  const float a0y = fmaf(g2.x, R0.x, fmaf(g2.y, R0.y, g2.z * R0.z));
+  const float a0z = fmaf(g3.x, R0.x, fmaf(g3.y, R0.y, g3.z * R0.z));
+  const float a1x = fmaf(g1.x, R1.x, fmaf(g1.y, R1.y, g1.z * R1.z));
+  const float a1y = fmaf(g2.x, R1.x, fmaf(g2.y, R1.y, g2.z * R1.z));
+  const float a1z = fmaf(g3.x, R1.x, fmaf(g3.y, R1.y, g3.z * R1.z));
+  const float al0 = fmaf(ux, a0x, fmaf(uy, a0y, uz * a0z));
+  const float al1 = fmaf(ux, a1x, fmaf(uy, a1y, uz * a1z));
+  // A_j = P N_j
+  const float b0x = fmaf(-al0, ux, a0x), b0y = fmaf(-al0, uy, a0y), b0z = fmaf(-al0, uz, a0z);
+  const float b1x = fmaf(-al1, ux, a1x), b1y = fmaf(-al1, uy, a1y), b1z = fmaf(-al1, uz, a1z);
+  const float k = rho2 - 1.f;
+  const float h00 = fmaf(k, fmaf(b0x, b0x, fmaf(b0y, b0y, b0z * b0z)), -al0 * al0);
+  const float h01 = fmaf(k, fmaf(b0x, b1x, fmaf(b0y, b1y, b0z * b1z)), -al0 * al1);
+  const float h11 = fmaf(k, fmaf(b1x, b1x, fmaf(b1y, b1y, b1z * b1z)), -al1 * al1);
+  const float det = fmaf(h00, h11, -h01 * h01);
+  if (!(h00 > 0.f && det > 1e-6f * h00 * h11)) return s;  // not a bounded ellipse
+  const float idet = 1.f / det;
+  const float alc = -sqrtf(rho2) / qz;  // y0^ . M R (z_c, 1) = y0^ . M (mu - o) / qz
+  // H^-1 beta
+  const float i0 = (h11 * al0 - h01 * al1) * idet, i1 = (h00 * al1 - h01 * al0) * idet;
+  const float D = alc * alc * (1.f + fmaf(al0, i0, al1 * i1));
+  if (!(D > 0.f)) return s;
+  const float iD = 1.f / D;
+  const float iqz = 1.f / qz;
+  const float cu = fmaf(alc, i0, qx * iqz), cv = fmaf(alc, i1, qy * iqz);
+  const float e00 = h00 * iD, e01 = h01 * iD, e11 = h11 * iD;
+  // tolerance: 2% + a 4e-6 error in the image-plane coordinates
+  const float lim = 1.02f + 8e-6f * sqrtf(e00 + e11);
+  s.c.x = cu;
+  s.c.y = cv;
+  s.h = make_float4(e00, 2.f * e01, e11, lim);
+  return s;
+}
+
+#if GSX_SCREEN_SMEM
+template <class Pre, int CH>
+__device__ inline void accumulate_list_cone(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
+                                            int count, bool want, int mc, float lo_t, float hi_t,
+                                            const SegBase& base, float dtf, const float* Y,
+                                            float (&sig)[CH], float (&W)[CH][3], Pre&& pre) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned a_pre = (unsigned)__cvta_generic_to_shared(sm.pre);
+  const float2 uv = sm.uv[lane];
+  for (int g = 0; g < count; g += 32) {
+    {
+      const int e = g + (int)lane;
+      const int64_t p = e < count ? (int64_t)sm.list[e] : 0;
+      const Silhouette S = prep_silhouette(sv, p, sm.cone[0], sm.camc);
+      sm.pre[lane] = S.c;
+      sm.pre[32 + lane] = S.h;
+    }
+    __syncwarp();
+    const int ng = count - g < 32 ? count - g : 32;
+#if GSX_SCREEN2
+    // screen the whole group first (independent tests, no votes), then visit
+    // only the entries some lane passes
+    unsigned mine = 0;
+#pragma unroll 4
+    for (int i = 0; i < ng; ++i) {
+      const float4 C = lds4(a_pre + 16u * (unsigned)i);
+      const float4 H = lds4(a_pre + 16u * (unsigned)(32 + i));
+      const float du = uv.x - C.x, dv = uv.y - C.y;
+      const float q = fmaf(du, fmaf(H.x, du, H.y * dv), H.z * dv * dv);
+      const bool pass = want && q <= H.w && C.z <= hi_t && C.w >= lo_t;
+      mine |= (pass ? 1u : 0u) << i;
+    }
+    PH_CNT(12, ng)
+    unsigned any = __reduce_or_sync(FULL, mine);
+    while (any) {
+      const int i = __ffs(any) - 1;
+      any &= any - 1;
+      const bool pass = (mine >> i) & 1u;
+      const int64_t p = sm.list[g + i];
+      pre(p, pass);
+      CandUse u = candidate_use(sv, r, p, pass, mc, base, dtf);
+      accumulate_used(sv, r, p, u, dtf, Y, sig, W);
+    }
+#else
+    for (int i = 0; i < ng; ++i) {
+      const float4 C = lds4(a_pre + 16u * (unsigned)i);
+      const float4 H = lds4(a_pre + 16u * (unsigned)(32 + i));
+      const float du = uv.x - C.x, dv = uv.y - C.y;
+      const float q = fmaf(du, fmaf(H.x, du, H.y * dv), H.z * dv * dv);
+      const bool pass = want && q <= H.w && C.z <= hi_t && C.w >= lo_t;
+      PH_CNT(12, 1)
+      if (!__any_sync(FULL, pass)) continue;
+      const int64_t p = sm.list[g + i];
+      pre(p, pass);
+      CandUse u = candidate_use(sv, r, p, pass, mc, base, dtf);
+      accumulate_used(sv, r, p, u, dtf, Y, sig, W);
+    }
+#endif
+    __syncwarp();
   }
 }
+
+#endif  // GSX_SCREEN_SMEM
+
+#if GSX_STAGE_N > 0
+__device__ inline void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ inline void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Pass 1 over a staged list with the candidates' geometry and appearance
+// (27 float4 = 432 B each) copied into shared memory GSX_STAGE_N entries at a
+// time, double-buffered with cp.async: the copies of the next group are in
+// flight (all 32 lanes, coalesced 16-byte pieces, L2 -> shared without
+// registers) while the current group is evaluated from shared memory, so the
+// per-entry chain no longer waits on two dependent L2 round trips (the list
+// index -> geometry -> setup -> appearance).  Same arithmetic, same order.
+template <class Pre, int CH>
+__device__ inline void accumulate_list_staged(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
+                                              int count, bool want, int mc, const SegBase& base,
+                                              float dtf, const float* Y, float (&sig)[CH],
+                                              float (&W)[CH][3], Pre&& pre) {
+  constexpr int NS = GSX_STAGE_N;
+  const int lane = (int)(threadIdx.x & 31);
+  auto issue = [&](int b, int g0) {
+    const int n = count - g0 < NS ? count - g0 : NS;
+    for (int k = lane; k < n * STAGE_F4; k += 32) {
+      const int e = k / STAGE_F4, j = k - e * STAGE_F4;
+      const int64_t p = sm.list[g0 + e];
+      const float4* src = j < 4 ? sv.geo + 4 * p + j : sv.app + GSX_APP_F4 * p + (j - 4);
+      cp_async16(&sm.stage[b][k], src);
+    }
+    cp_async_commit();
+  };
+  if (count <= 0) return;
+  issue(0, 0);
+  int b = 0;
+  for (int g0 = 0; g0 < count; g0 += NS) {
+    if (g0 + NS < count) {
+      issue(b ^ 1, g0 + NS);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int n = count - g0 < NS ? count - g0 : NS;
+    for (int e = 0; e < n; ++e) {
+      const int64_t p = sm.list[g0 + e];
+      pre(p, want);
+      const float4* st = sm.stage[b] + e * STAGE_F4;
+      const CandUse u = candidate_use_at<SmemLoad>(st, r, want, mc, base, dtf);
+      accumulate_used_at<SmemLoad>(st + 4, r, u, dtf, Y, sig, W);
+    }
+    __syncwarp();
+    b ^= 1;
+  }
+}
+#endif  // GSX_STAGE_N
 
 // Exact AABB-emptiness of the lane's segment (reference semantics) after the
 // true-intersection pass; STATS additionally counts every exact overlap.
