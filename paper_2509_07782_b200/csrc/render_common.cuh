@@ -142,11 +142,18 @@ struct SmemLoad {
   }
 };
 
+// SH basis of a lane kept in shared memory (stride 32 floats: one column per
+// lane), so the 9 values do not occupy registers across the march
+struct YSmem {
+  const float* p;
+  __device__ float operator[](int b) const { return p[32 * b]; }
+};
+
 // unclamped radiance and lobe values (lobes may be NULL); app = GSX_APP_F4
 // float4 in the streaming layout, consumed one float4 at a time so the
 // coefficients never need 76 live registers.
-template <class L = LdgLoad>
-__device__ inline void eval_radiance_pre(const float4* __restrict__ app, const float* Y,
+template <class L = LdgLoad, class YT = const float*>
+__device__ inline void eval_radiance_pre(const float4* __restrict__ app, YT Y,
                                          const float* d, float* pre, float* lobes) {
   float s0 = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -171,11 +178,11 @@ __device__ inline void eval_radiance_pre(const float4* __restrict__ app, const f
   pre[2] = s2;
 }
 
-template <class L = LdgLoad>
-__device__ inline void eval_radiance_f(const float4* __restrict__ app, const float* Y,
+template <class L = LdgLoad, class YT = const float*>
+__device__ inline void eval_radiance_f(const float4* __restrict__ app, YT Y,
                                        const float* d, float* c) {
   float pre[3];
-  eval_radiance_pre<L>(app, Y, d, pre, nullptr);
+  eval_radiance_pre<L, YT>(app, Y, d, pre, nullptr);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) c[ch] = fmaxf(pre[ch], 0.f);
 }

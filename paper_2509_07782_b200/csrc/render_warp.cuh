@@ -22,6 +22,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GSX_SYNC_FWD
 #define GSX_SYNC_FWD 1.0f
 #endif
+// uniform mode (short fixed segments; packet-cone traversal): C2 15.6 ms at
+// 0.5 vs 17.4 at 1.0 (C3, adaptive: 33.3 at 0.5, 31.1 at 1.0, 31.8 at 2.0)
+#ifndef GSX_SYNC_FWD_U
+#define GSX_SYNC_FWD_U 0.5f
+#endif
 #ifndef GSX_SYNC_BWD
 #define GSX_SYNC_BWD 0.5f
 #endif
@@ -71,6 +76,9 @@ struct Counters {
 #ifndef GSX_STAGE_N
 #define GSX_STAGE_N 0
 #endif
+#ifndef GSX_Y_SMEM
+#define GSX_Y_SMEM 0
+#endif
 constexpr int STAGE_F4 = 4 + GSX_APP_F4;
 struct WarpSmem {
   int32_t stack[WSTACK];
@@ -83,6 +91,9 @@ struct WarpSmem {
 #endif
 #if GSX_STAGE_N > 0
   float4 stage[2][GSX_STAGE_N * STAGE_F4];
+#endif
+#if GSX_Y_SMEM
+  float ylane[9][32];  // per-lane SH basis (forward)
 #endif
 };
 
@@ -576,9 +587,9 @@ __device__ inline CandUse candidate_use(const SceneView& sv, const RayCtx& r, in
 
 // Pass-1 accumulation of one candidate into the 16 per-sample sums
 // (renderer.py:218-228), given its setup.
-template <class L = LdgLoad, int CH = 16>
+template <class L = LdgLoad, int CH = 16, class YT = const float*>
 __device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, const CandUse& u,
-                                          float dtf, const float* Y, float (&sig)[CH],
+                                          float dtf, YT Y, float (&sig)[CH],
                                           float (&W)[CH][3]) {
   const CandSetup& cs = u.cs;
   const bool use = u.use;
@@ -588,7 +599,7 @@ __device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, co
   if (!__any_sync(FULL, use)) return false;
   PH_CNT(14, 1)
   float c[3] = {0.f, 0.f, 0.f};
-  if (use) eval_radiance_f<L>(app, Y, r.df, c);
+  if (use) eval_radiance_f<L, YT>(app, Y, r.df, c);
   const float nkl2 = -cs.kl2;
   // 4-sample groups outside every lane's range are skipped warp-uniformly
 #pragma unroll
@@ -612,17 +623,17 @@ __device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, co
   return true;
 }
 
-template <int CH>
+template <int CH, class YT>
 __device__ inline bool accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
-                                       const CandUse& u, float dtf, const float* Y,
+                                       const CandUse& u, float dtf, YT Y,
                                        float (&sig)[CH], float (&W)[CH][3]) {
   return accumulate_used_at(sv.app + GSX_APP_F4 * p, r, u, dtf, Y, sig, W);
 }
 
-template <int CH>
+template <int CH, class YT>
 __device__ inline bool accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
                                             bool want, int mc, const SegBase& base, float dtf,
-                                            const float* Y, float (&sig)[CH],
+                                            YT Y, float (&sig)[CH],
                                             float (&W)[CH][3]) {
   const CandUse u = candidate_use(sv, r, p, want, mc, base, dtf);
   return accumulate_used(sv, r, p, u, dtf, Y, sig, W);
@@ -633,10 +644,10 @@ __device__ inline bool accumulate_candidate(const SceneView& sv, const RayCtx& r
 // COMPACT: the list is compacted in place to the entries some lane used (the
 // only ones with a non-zero contribution, hence the only ones the logged
 // backward needs); returns the new count.
-template <bool COMPACT = false, class Pre, int CH>
+template <bool COMPACT = false, class Pre, int CH, class YT>
 __device__ inline int accumulate_list(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
                                       int count, bool want, int mc, const SegBase& base,
-                                      float dtf, const float* Y, float (&sig)[CH],
+                                      float dtf, YT Y, float (&sig)[CH],
                                       float (&W)[CH][3], Pre&& pre) {
   // (L1 prefetch of the listed geometry / appearance blocks measured slower:
   // 40.9 vs 40.0 ms on C3 -- the entry loop is not load-latency bound)
@@ -751,10 +762,10 @@ __device__ inline Silhouette prep_silhouette(const SceneView& sv, int64_t p, con
 }
 
 #if GSX_SCREEN_SMEM
-template <class Pre, int CH>
+template <class Pre, int CH, class YT>
 __device__ inline void accumulate_list_cone(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
                                             int count, bool want, int mc, float lo_t, float hi_t,
-                                            const SegBase& base, float dtf, const float* Y,
+                                            const SegBase& base, float dtf, YT Y,
                                             float (&sig)[CH], float (&W)[CH][3], Pre&& pre) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned a_pre = (unsigned)__cvta_generic_to_shared(sm.pre);
@@ -834,10 +845,10 @@ __device__ inline void cp_async_wait() {
 // registers) while the current group is evaluated from shared memory, so the
 // per-entry chain no longer waits on two dependent L2 round trips (the list
 // index -> geometry -> setup -> appearance).  Same arithmetic, same order.
-template <class Pre, int CH>
+template <class Pre, int CH, class YT>
 __device__ inline void accumulate_list_staged(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
                                               int count, bool want, int mc, const SegBase& base,
-                                              float dtf, const float* Y, float (&sig)[CH],
+                                              float dtf, YT Y, float (&sig)[CH],
                                               float (&W)[CH][3], Pre&& pre) {
   constexpr int NS = GSX_STAGE_N;
   const int lane = (int)(threadIdx.x & 31);
