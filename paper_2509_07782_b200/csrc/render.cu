@@ -6,19 +6,30 @@
 // One thread per ray; a CTA renders one 16x16 tile with pixels in Z-order
 // (each warp = an 8x4 pixel block, so its 32 rays are spatially coherent).
 // The warp marches in lockstep, one segment per lane per iteration ("slab by
-// slab", render_warp.cuh): a warp-cooperative traversal of the 4-wide BVH
-// over the union of the 32 segments (fp32 slab tests, conservative margin)
-// stages the candidates in a shared-memory list; every lane then evaluates
-// the list against its own ray: an fp32 per-(ray, primitive) setup relative
-// to the segment's base point reduces the density along the ray to
-// q(t) = A (t - t_c)^2 + q_min, and the 16 samples of the segment accumulate
-// in registers with one FMA pair + one EX2 per (sample, primitive).
-// AABB-emptiness (which drives empty-space skipping) is decided with the
-// reference's exact fp64 slab test on the candidates, so ESS jumps and
-// adaptive grid restarts happen exactly where the reference's do.
-// the forward measured faster with the cold paths inlined (C3: 40.3 vs 41.2 ms)
-// Cold fp64 paths (phantom probe, exact AABB test, closest-hit leaf test)
-// inlined: C3 32.9 ms vs 38.2 out of line (cone traversal, no screen).
+// slab", render_warp.cuh).  Camera rays share one origin, so the taking-part
+// lanes' segments lie in a cone cut by a distance shell: a warp-cooperative
+// traversal of the 4-wide BVH tests that cone against one child box per lane
+// (8 nodes per step) and stages the leaves in a shared-memory list
+// (warp_traverse_cone; explicit-ray batches use the per-lane packet test,
+// warp_traverse).  Every lane then evaluates the list against its own ray:
+// an fp32 per-(ray, primitive) setup relative to the segment's base point
+// reduces the density along the ray to q(t) = A (t - t_c)^2 + q_min, and the
+// 16 samples of the segment accumulate in registers with one FMA pair + one
+// EX2 per (sample, primitive).  AABB-emptiness (which drives empty-space
+// skipping) is decided with the reference's exact fp64 slab test on the
+// candidates, so ESS jumps and adaptive grid restarts happen exactly where
+// the reference's do.
+//
+// Tuning (C3 / C2 ms on one B200, A/B on the same box, profiles/
+// time_variants.py):
+//  * cold fp64 paths (exact AABB test, closest-hit leaf test, phantom probe)
+//    inlined: C3 32.9 vs 38.2 out of line;
+//  * per-lane SH basis in shared memory (GSX_Y_SMEM): 31.15 vs 31.28;
+//  * packet cone for every camera render, logged (training) one included:
+//    C3 31.2 vs 34.7 per-lane packet; C2 17.5 vs 17.2 at equal depth-sync;
+//  * rejected: 8-sample chunks (C3 38.0), persistent warps (+0.2), gating
+//    the exact test by the lane's own use (C3 -1.5%, C2 +4%), the silhouette
+//    screen and cp.async staging (profiles/experiments/).
 #ifndef GSX_COLD
 #define GSX_COLD inline
 #endif
@@ -28,26 +39,16 @@
 #ifndef GSX_CHLEAF_ATTR
 #define GSX_CHLEAF_ATTR inline
 #endif
-#ifndef GSX_CONE_SCREEN
-#define GSX_CONE_SCREEN 0
-#endif
-#define GSX_SCREEN_SMEM GSX_CONE_SCREEN
-// staged (cp.async double-buffered) candidate data: measured slower (C3
-// 35.5 vs 32.9 ms, C2 19.7 vs 18.3): off
-#ifndef GSX_STAGE_N
-#define GSX_STAGE_N 0
-#endif
 #ifndef GSX_Y_SMEM
 #define GSX_Y_SMEM 1
 #endif
-// (Gating the exact AABB test by the lane's own use of the entry, with the
-// rest of the list as fallback: C3 -1.5%, C2 +4% -- not kept.)
 // camera-kernel traversal: 0 per-lane packet (warp_traverse), 1 packet cone
-// (warp_traverse_cone), 2 cone for the plain forward, per-lane packet for the
-// logged (training) forward
+// (warp_traverse_cone), 2 cone for the plain forward only
 #ifndef GSX_FWD_CONE
 #define GSX_FWD_CONE 1
 #endif
+// samples per chunk of the plain forward (n_s > CH: several chunks, each
+// traversing its share of the segment)
 #ifndef GSX_FWD_CH
 #define GSX_FWD_CH 16
 #endif
@@ -116,7 +117,6 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       if (!STATS && gate && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
     };
-    bool single = true;
     for (;;) {
       PH_BEGIN(ph_t)
       if (CONE)
@@ -125,29 +125,13 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
         warp_traverse(bv, r, wch, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
       PH_END(1, ph_t)
       PH_BEGIN(ph_p)
-#if GSX_CONE_SCREEN
-      if (CONE)
-        accumulate_list_cone(sv, r, sm, count, wch, mc, lim.lo_t, lim.hi_t, base, dtf, Y, sig, W,
-                             exact);
-      else
-#endif
-#if GSX_STAGE_N > 0
-        accumulate_list_staged(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
-#else
-        // the logged forward records only the entries some lane used
-        count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
-#endif
+      // the logged forward records only the entries some lane used
+      count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
       PH_END(2, ph_p)
       if (CONE ? cst.done : st.done) break;
-      single = false;
       if (save) log_list_chunk(lw, sm.list, count);
       __syncwarp();
       count = 0;
-    }
-    if (CONE && GSX_CONE_SCREEN && !STATS && single && wch && !nonempty) {
-      // the screen gated the exact test: lanes without a screened overlap
-      // test the whole (single-chunk) list before emptiness_tail's probe
-      for (int i = 0; i < count && !nonempty; ++i) exact(sm.list[i], true);
     }
     if constexpr (SAVE) {
       if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
@@ -249,19 +233,6 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
   RayAccum acc;
   acc.init();
   LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
-#if GSX_CONE_SCREEN
-  {
-    // image-plane coordinates of the lane's pixel and the camera columns for
-    // the silhouette screen (accumulate_list_cone)
-    const float inv_f = (float)(1.0 / cam.focal);
-    sw.uv[lane] = make_float2(((float)px + 0.5f - 0.5f * (float)W) * inv_f,
-                              ((float)py + 0.5f - 0.5f * (float)H) * inv_f);
-    if (lane < 3)
-      sw.camc[lane] =
-          make_float4((float)cam.R[lane], (float)cam.R[3 + lane], (float)cam.R[6 + lane], 0.f);
-    __syncwarp();
-  }
-#endif
   march_forward<STATS, SAVE, FWD_CONE(SAVE)>(sv, bv, r, hit, cfg, acc, cnt, sw, lw);
   if (SAVE) log_finish(lw, log_nw);
   if (valid) {
