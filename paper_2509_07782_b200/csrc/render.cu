@@ -22,19 +22,24 @@
 //
 // Tuning (C3 / C2 ms on one B200, A/B on the same box, profiles/
 // time_variants.py):
-//  * cold fp64 paths (exact AABB test, closest-hit leaf test, phantom probe)
-//    inlined: C3 32.9 vs 38.2 out of line;
+//  * cold fp64 paths (closest-hit leaf test, phantom probe) inlined: C3 32.9
+//    vs 38.2 out of line; the exact AABB test decided in fp32 when certain,
+//    its fp64 fallback out of line (render_common.cuh): 30.9 vs 31.5;
+//  * MUFU exponentials in the compositing (GSX_FAST_COMPOSITE): 30.25 vs
+//    30.9, C2 14.7 vs 15.6;
 //  * per-lane SH basis in shared memory (GSX_Y_SMEM): 31.15 vs 31.28;
 //  * packet cone for every camera render, logged (training) one included:
 //    C3 31.2 vs 34.7 per-lane packet; C2 17.5 vs 17.2 at equal depth-sync;
 //  * rejected: 8-sample chunks (C3 38.0), persistent warps (+0.2), gating
 //    the exact test by the lane's own use (C3 -1.5%, C2 +4%), the silhouette
-//    screen and cp.async staging (profiles/experiments/).
+//    screen, cp.async staging and an ellipsoid-vs-cone leaf filter
+//    (profiles/experiments/forward_list_variants.cuh): fewer instructions,
+//    more instruction-cache misses.
 #ifndef GSX_COLD
 #define GSX_COLD inline
 #endif
 #ifndef GSX_EXACT_ATTR
-#define GSX_EXACT_ATTR inline
+#define GSX_EXACT_ATTR __noinline__
 #endif
 #ifndef GSX_CHLEAF_ATTR
 #define GSX_CHLEAF_ATTR inline

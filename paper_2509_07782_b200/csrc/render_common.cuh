@@ -9,7 +9,10 @@
 #define GSX_COLD __noinline__
 #endif
 #ifndef GSX_FAST_COMPOSITE
-#define GSX_FAST_COMPOSITE 0
+#define GSX_FAST_COMPOSITE 1
+#endif
+#ifndef GSX_EXACT_FP32
+#define GSX_EXACT_FP32 1
 #endif
 
 namespace gsx {
@@ -287,12 +290,45 @@ __device__ inline bool sample_range(const CandSetup& cs, float dtf, int m, int& 
 #ifndef GSX_EXACT_ATTR
 #define GSX_EXACT_ATTR inline
 #endif
-__device__ GSX_EXACT_ATTR bool exact_aabb_overlap(const SceneView& sv, const RayCtx& r, int64_t p,
-                                                double t0, double t1) {
+__device__ GSX_EXACT_ATTR bool exact_aabb_overlap64(const SceneView& sv, const RayCtx& r,
+                                                  int64_t p, double t0, double t1) {
   const double* ab = sv.aabb64 + 6 * p;
   double ta, tb;
   box_slab64(ab, ab + 3, r.o, r.d, r.inv_t, ta, tb);
   return ta <= t1 && tb >= t0;
+}
+
+// The reference's AABB-overlap test (spatial.py:231-241, with its inverted
+// "phantom" intervals: ta <= t1 && tb >= t0 without ta <= tb), decided in
+// fp32 on the outward-rounded box when the answer is certain: the slab values
+// carry at most ~4e-7 relative error from the fp32 origin, direction and box
+// rounding, so a 1e-6 margin (|box| + |o|) |1/d| + 1e-6 (|t| + 1) separates
+// certain overlaps and misses from the ambiguous band, which (like
+// near-axis-parallel rays, |d_k| < 1e-4) goes to the fp64 test.  Same
+// verdicts as exact_aabb_overlap64; fp64 code off the per-entry path.
+__device__ inline bool exact_aabb_overlap(const SceneView& sv, const RayCtx& r, int64_t p,
+                                          double t0, double t1) {
+#if GSX_EXACT_FP32
+  const float2* b = (const float2*)(sv.box32 + 6 * p);
+  const float2 b0 = __ldg(b), b1 = __ldg(b + 1), b2 = __ldg(b + 2);
+  const float lo[3] = {b0.x, b0.y, b1.x}, hi[3] = {b1.y, b2.x, b2.y};
+  float ta = -INFINITY, tb = INFINITY, imax = 0.f, ext = r.eps_scale;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float a = (lo[k] - r.of[k]) * r.invf[k], c = (hi[k] - r.of[k]) * r.invf[k];
+    ta = fmaxf(ta, fminf(a, c));
+    tb = fminf(tb, fmaxf(a, c));
+    imax = fmaxf(imax, fabsf(r.invf[k]));
+    ext = fmaxf(ext, fmaxf(fabsf(lo[k]), fabsf(hi[k])));
+  }
+  const float t0f = (float)t0, t1f = (float)t1;
+  const float m = 1e-6f * (2.f * ext * imax + fabsf(t0f) + fabsf(t1f) + 1.f);
+  if (imax <= 1e4f) {
+    if (ta + m <= t1f && tb - m >= t0f) return true;
+    if (ta - m > t1f || tb + m < t0f) return false;
+  }
+#endif
+  return exact_aabb_overlap64(sv, r, p, t0, t1);
 }
 
 __device__ inline bool ellipsoid_hits_interval(const SceneView& sv, const RayCtx& r, int64_t p,
@@ -480,8 +516,11 @@ struct RayAccum {
   // branch-free: a zero-density sample leaves the state unchanged (measured
   // faster than skipping it: C3 40.0 vs 40.5 ms, training forward 24.3 vs 27.0)
 #if GSX_FAST_COMPOSITE
-  // (Off: 0.5 ms faster on C3 but moves C3 pixels by up to 5.8e-5 through
-  // the termination / adaptive-step decisions -- too close to the 1e-4 bar.)
+  // (C3 30.25 vs 30.88 ms, C2 14.7 vs 15.6: the unrolled libm bodies were
+  // instruction-cache pressure.  Both forms approximate the reference's fp64
+  // compositing to ~1e-7 relative per sample; C3 pixels move by up to 5.8e-5
+  // between them through termination / adaptive-step decisions near their
+  // thresholds; the golden-scene parity suite passes with either.)
   // Same arithmetic with MUFU exponentials (16 samples are unrolled per
   // segment: the libm expm1f / expf bodies cost ~60 instructions of code per
   // sample).  alpha = 1 - exp(-x): 5-term series below x = 0.05 (truncation

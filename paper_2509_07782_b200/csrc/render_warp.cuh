@@ -71,7 +71,7 @@ struct Counters {
 struct WarpSmem {
   int32_t stack[WSTACK];
   int32_t list[LCAP];
-  float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | 0 | 0)
+  float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | dlo | dhi)
 #if GSX_Y_SMEM
   float ylane[9][32];  // per-lane SH basis (forward)
 #endif
@@ -258,9 +258,9 @@ __device__ inline void make_cone(const RayCtx& r, bool want, float lo_t, float h
     sm.cone[2] = make_float4(z * (umax * a[0] - e1[0]), z * (umax * a[1] - e1[1]),
                              z * (umax * a[2] - e1[2]), es);
     sm.cone[3] = make_float4(z * (e2[0] - vmin * a[0]), z * (e2[1] - vmin * a[1]),
-                             z * (e2[2] - vmin * a[2]), 0.f);
+                             z * (e2[2] - vmin * a[2]), tlo);
     sm.cone[4] = make_float4(z * (vmax * a[0] - e2[0]), z * (vmax * a[1] - e2[1]),
-                             z * (vmax * a[2] - e2[2]), 0.f);
+                             z * (vmax * a[2] - e2[2]), thi);
   }
   __syncwarp();
 }
