@@ -22,8 +22,8 @@
 //
 // Tuning (C3 / C2 ms on one B200, A/B on the same box, profiles/
 // time_variants.py):
-//  * cold fp64 paths (closest-hit leaf test, phantom probe) inlined: C3 32.9
-//    vs 38.2 out of line; the exact AABB test decided in fp32 when certain,
+//  * cold fp64 paths inlined: C3 32.9 vs 38.2 all out of line -- except the
+//    closest-hit leaf test (below); the exact AABB test decided in fp32 when certain,
 //    its fp64 fallback out of line (render_common.cuh): 30.9 vs 31.5;
 //  * MUFU exponentials in the compositing (GSX_FAST_COMPOSITE): 30.25 vs
 //    30.9, C2 14.7 vs 15.6;
@@ -41,8 +41,10 @@
 #ifndef GSX_EXACT_ATTR
 #define GSX_EXACT_ATTR __noinline__
 #endif
+// closest-hit leaf test (fp64 division / square root bodies) out of line:
+// C2 14.0 vs 14.5 ms, C3 29.6 vs 29.8 (with rcbrt in segment_step)
 #ifndef GSX_CHLEAF_ATTR
-#define GSX_CHLEAF_ATTR inline
+#define GSX_CHLEAF_ATTR __noinline__
 #endif
 #ifndef GSX_Y_SMEM
 #define GSX_Y_SMEM 1

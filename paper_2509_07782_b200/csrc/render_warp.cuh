@@ -197,15 +197,17 @@ __device__ inline void sts_i_if(unsigned a, int32_t v, bool p) {
                "r"(v), "r"((unsigned)p)
                : "memory");
 }
+// warp-wide fp32 min / max: one redux.sync (sm_100a CREDUX.F32, result in a
+// uniform register) instead of a 5-step shuffle tree
 __device__ inline float warp_min(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fminf(x, __shfl_xor_sync(FULL, x, o));
-  return x;
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+  return r;
 }
 __device__ inline float warp_max(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(FULL, x, o));
-  return x;
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // Build the cone of the lanes with `want` (at least one) over [lo_t, hi_t]
@@ -811,9 +813,7 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
     bool go = active;
     if (sync > 0.f) {
       float t0f = active ? (float)seg.t0 : INFINITY;
-      float dmin = t0f;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(FULL, dmin, o));
+      const float dmin = warp_min(t0f);
       go = active && t0f <= dmin + sync * (float)(seg.t1 - seg.t0);
     }
     PH_CNT(10, 1)
