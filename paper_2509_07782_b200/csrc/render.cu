@@ -59,6 +59,10 @@
 #ifndef GSX_FWD_CH
 #define GSX_FWD_CH 16
 #endif
+// ESS closest hit by cone windows (warp_closest_hit_cone)
+#ifndef GSX_CONE_CH
+#define GSX_CONE_CH 1
+#endif
 #define FWD_CONE(save) (GSX_FWD_CONE == 1 || (GSX_FWD_CONE == 2 && !(save)))
 #include "gsx_common.cuh"
 #include "march_log.cuh"
@@ -198,7 +202,7 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
   const float* Yv = Y;
 #endif
   const int ns = (int)cfg.n_s;
-  march_warp<STATS>(sv, bv, r, hit, cfg, acc, cnt, cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sm, [&](const Seg& seg, bool want) {
+  march_warp<STATS, CONE && GSX_CONE_CH>(sv, bv, r, hit, cfg, acc, cnt, cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sm, [&](const Seg& seg, bool want) {
     return forward_segment<STATS, SAVE, CONE>(sv, bv, r, want, seg, ns, Yv, acc, cnt, sm, lw);
   });
 }

@@ -317,36 +317,52 @@ __device__ inline void cone_begin(WarpSmem& sm, ConeTrav& st) {
 // (st.done) or the list has fewer than 32 free entries.  The number of nodes
 // popped shrinks as the stack fills (a step pushes at most 3 more than it
 // pops), so the 256-entry stack overflows only for trees deeper than ~80.
+#ifndef GSX_CONE_CPL
+#define GSX_CONE_CPL 1  // children per lane and step (8 * CPL nodes per step)
+#endif
 __device__ inline void warp_traverse_cone(const BvhView& bv, ConeTrav& st, WarpSmem& sm,
                                           int& count, uint32_t& visits) {
+  constexpr int CPL = GSX_CONE_CPL, KMAX = 8 * CPL;
   const unsigned a_list = (unsigned)__cvta_generic_to_shared(sm.list);
   const unsigned a_stack = (unsigned)__cvta_generic_to_shared(sm.stack);
   const unsigned a_cone = (unsigned)__cvta_generic_to_shared(sm.cone);
   const unsigned lane = threadIdx.x & 31, lt = lanemask_lt();
   const int slot = (int)(lane >> 2), c = (int)(lane & 3);
-  while (st.sp > 0 && count <= LCAP - 32) {
-    int k = st.sp < 8 ? st.sp : 8;
+  while (st.sp > 0 && count <= LCAP - 32 * CPL) {
+    int k = st.sp < KMAX ? st.sp : KMAX;
     const int room = (WSTACK - st.sp) / 3;
     k = k < room ? k : (room > 1 ? room : 1);
     const int base = st.sp - k;
     visits += (uint32_t)k;
     PH_CNT(8, k)
-    const bool valid = slot < k;
-    const int32_t node = valid ? lds_i(a_stack + 4u * (unsigned)(base + slot)) : 0;
-    const float* nf = (const float*)(bv.nodes4 + 8 * (int64_t)node);
-    const int32_t ch = __float_as_int(__ldg(nf + 24 + c));
-    // (absent children have inf / -inf boxes: NaN centres fail every test)
-    const bool cb = cone_box(a_cone, __ldg(nf + c), __ldg(nf + 4 + c), __ldg(nf + 8 + c),
-                             __ldg(nf + 12 + c), __ldg(nf + 16 + c), __ldg(nf + 20 + c));
-    const bool hit = valid && ch != GSX_NONE && cb;
-    const bool leaf = hit && ch < 0, inner = hit && ch >= 0;
-    const unsigned bl = __ballot_sync(FULL, leaf), bi = __ballot_sync(FULL, inner);
-    sts_i_if(a_list + 4u * (unsigned)(count + __popc(bl & lt)), ~ch, leaf);
-    const int pos = base + __popc(bi & lt);
-    sts_i_if(a_stack + 4u * (unsigned)pos, ch, inner && pos < WSTACK);
-    count += __popc(bl);
-    const int np = base + __popc(bi);
-    st.sp = np < WSTACK ? np : WSTACK;
+    int32_t chv[CPL];
+    bool hitv[CPL];
+#pragma unroll
+    for (int h = 0; h < CPL; ++h) {
+      const int sl = slot + 8 * h;
+      const bool valid = sl < k;
+      const int32_t node = valid ? lds_i(a_stack + 4u * (unsigned)(base + sl)) : 0;
+      const float* nf = (const float*)(bv.nodes4 + 8 * (int64_t)node);
+      chv[h] = __float_as_int(__ldg(nf + 24 + c));
+      // (absent children have inf / -inf boxes: NaN centres fail every test)
+      const bool cb = cone_box(a_cone, __ldg(nf + c), __ldg(nf + 4 + c), __ldg(nf + 8 + c),
+                               __ldg(nf + 12 + c), __ldg(nf + 16 + c), __ldg(nf + 20 + c));
+      hitv[h] = valid && chv[h] != GSX_NONE && cb;
+    }
+    int sp = base;
+#pragma unroll
+    for (int h = 0; h < CPL; ++h) {
+      const int32_t ch = chv[h];
+      const bool leaf = hitv[h] && ch < 0, inner = hitv[h] && ch >= 0;
+      const unsigned bl = __ballot_sync(FULL, leaf), bi = __ballot_sync(FULL, inner);
+      sts_i_if(a_list + 4u * (unsigned)(count + __popc(bl & lt)), ~ch, leaf);
+      const int pos = sp + __popc(bi & lt);
+      sts_i_if(a_stack + 4u * (unsigned)pos, ch, inner && pos < WSTACK);
+      count += __popc(bl);
+      const int np = sp + __popc(bi);
+      sp = np < WSTACK ? np : WSTACK;
+    }
+    st.sp = sp;
     __syncwarp();
   }
   st.done = st.sp == 0;
@@ -490,6 +506,77 @@ __device__ inline bool warp_closest_hit(const SceneView& sv, const BvhView& bv, 
     node = next;
   }
   __syncwarp();
+  if (want && best < INFINITY) {
+    hit = best;
+    return true;
+  }
+  return false;
+}
+
+// fp32 true ray/box intersection of primitive p's outward-rounded box with
+// [lo_t, hi_t] (margins included by the caller; gap as in traverse_segment)
+__device__ inline bool box32_hit(const SceneView& sv, const RayCtx& r, int64_t p, float lo_t,
+                                 float hi_t, float gap) {
+  const float2* b = (const float2*)(sv.box32 + 6 * p);
+  const float2 b0 = __ldg(b), b1 = __ldg(b + 1), b2 = __ldg(b + 2);
+  const float x0 = (b0.x - r.of[0]) * r.invf[0], x1 = (b1.y - r.of[0]) * r.invf[0];
+  const float y0 = (b0.y - r.of[1]) * r.invf[1], y1 = (b2.x - r.of[1]) * r.invf[1];
+  const float z0 = (b1.x - r.of[2]) * r.invf[2], z1 = (b2.y - r.of[2]) * r.invf[2];
+  const float mn = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fminf(z0, z1));
+  const float mx = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fmaxf(z0, z1));
+  return mn <= hi_t && mx >= lo_t && mn <= mx + gap;
+}
+
+// Cone-window ESS closest hit (camera rays; closest_hit spatial.py:309-354):
+// the requesting lanes search depth windows [A, A + w), w doubling, each by a
+// packet-cone traversal of the window; every listed leaf whose box a lane's
+// ray truly meets (fp32, margins) gets the lane's fp64 leaf test.  A lane is
+// done once its best entry is <= the window end: every ellipsoid its ray
+// meets in [t_lo, B] has its box in one of the windows' cones, so no
+// undiscovered one can enter earlier.  The minimum over the same fp64 leaf
+// tests as warp_closest_hit, hence the same hit bit for bit.
+__device__ inline bool warp_closest_hit_cone(const SceneView& sv, const BvhView& bv,
+                                             const RayCtx& r, bool want, double t_lo,
+                                             double t_hi, double& hit, WarpSmem& sm,
+                                             uint32_t& visits) {
+  want = want && !(t_lo > t_hi);
+  if (!__any_sync(FULL, want)) return false;
+  double best = INFINITY;
+  bool pend = want;
+  float A = warp_min(want ? (float)t_lo : INFINITY);
+  float w = warp_max(want ? (float)(t_hi - t_lo) * (1.f / 64.f) : 0.f);
+  while (__any_sync(FULL, pend)) {
+    w = fmaxf(w, 1e-6f * (fabsf(A) + 1.f));
+    const float B = A + w;
+    const double lim = t_hi < best ? t_hi : best;
+    float lo = fmaxf((float)t_lo, A), hi = fminf((float)lim, B);
+    lo -= margin(r, lo);
+    hi += margin(r, hi);
+    const bool part = pend && lo <= hi;
+    if (__any_sync(FULL, part)) {
+      make_cone(r, part, lo, hi, sm);
+      ConeTrav st;
+      cone_begin(sm, st);
+      int count = 0;
+      const float blo = (float)t_lo - margin(r, (float)t_lo);
+      for (;;) {
+        warp_traverse_cone(bv, st, sm, count, visits);
+        for (int i = 0; i < count; ++i) {
+          const int64_t p = sm.list[i];
+          const double l2 = t_hi < best ? t_hi : best;
+          const float bhi = (float)l2 + margin(r, (float)l2);
+          if (part && box32_hit(sv, r, p, blo, bhi, margin(r, bhi)))
+            best = ch_leaf(sv, p, r, t_lo, t_hi, best);
+        }
+        __syncwarp();
+        if (st.done) break;
+        count = 0;
+      }
+    }
+    pend = pend && !(best <= (double)B) && t_hi > (double)B;
+    A = B;
+    w *= 2.f;
+  }
   if (want && best < INFINITY) {
     hit = best;
     return true;
@@ -728,7 +815,7 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
 // exact AABB-emptiness verdict (true = non-empty).
 // `sync` = depth-synchronous window in segment lengths (0 = every active lane
 // takes part every iteration).
-template <bool STATS, class SegFn>
+template <bool STATS, bool CONE_CH = false, class SegFn>
 __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                   bool hit, const gsx_render_cfg& cfg, const RayAccum& acc,
                                   Counters<STATS>& cnt, float sync, WarpSmem& sm,
@@ -755,7 +842,9 @@ __device__ inline void march_warp(const SceneView& sv, const BvhView& bv, const 
     PH_BEGIN(ph_ch)
     if (__any_sync(FULL, need_ch)) {
       double h = 0.0;
-      const bool got = warp_closest_hit(sv, bv, r, need_ch, ch_from, t_f, h, sm, visits);
+      const bool got =
+          CONE_CH ? warp_closest_hit_cone(sv, bv, r, need_ch, ch_from, t_f, h, sm, visits)
+                  : warp_closest_hit(sv, bv, r, need_ch, ch_from, t_f, h, sm, visits);
       if (need_ch) {
         if (STATS) cnt.ch_calls++;
         if (!got) {
