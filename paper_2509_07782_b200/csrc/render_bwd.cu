@@ -183,7 +183,7 @@ __device__ inline void sample_adjoint(RayAccum& acc, const PixelGrad& pg, float 
   acc.add_sample(sj, Wj, tj, dtf);
   if (sj > 0.f) {
     const float ods = sj * dtf;
-    const float w = -expm1f(-ods) * Tj;  // the forward's w_j
+    const float w = RayAccum::alpha(ods) * Tj;  // the forward's w_j
     const float s = w / sj;
     const float cgj = (pg.gC[0] * Wj[0] + pg.gC[1] * Wj[1] + pg.gC[2] * Wj[2]) / sj;
     const float after = pg.gC[0] * (pg.Ctot[0] - acc.C[0]) + pg.gC[1] * (pg.Ctot[1] - acc.C[1]) +

@@ -536,13 +536,17 @@ struct RayAccum {
   // < x^6/720 = 2e-11 relative), else 1 - 2^(-x log2 e) (ex2.approx relative
   // error ~1e-7, i.e. < 2.4e-6 relative on alpha >= 0.049); T = 2^(-od log2 e)
   // to ~2e-7 relative.
-  __device__ void add_sample(float sig, const float* W, float tj, float dt) {
-    const bool on = sig > 0.f;
-    const float x = on ? sig * dt : 0.f;
+  // opacity 1 - exp(-x) of a sample with optical depth x >= 0
+  __device__ static float alpha(float x) {
     const float ser =
         x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.f / 120.f, -1.f / 24.f), 1.f / 6.f), -0.5f), 1.f);
     const float big = 1.f - ex2_approx(-1.4426950408889634f * x);
-    const float w = (x < 0.05f ? ser : big) * T;
+    return x < 0.05f ? ser : big;
+  }
+  __device__ void add_sample(float sig, const float* W, float tj, float dt) {
+    const bool on = sig > 0.f;
+    const float x = on ? sig * dt : 0.f;
+    const float w = alpha(x) * T;
     const float s = on ? __fdividef(w, sig) : 0.f;
     C[0] = fmaf(s, W[0], C[0]);
     C[1] = fmaf(s, W[1], C[1]);
@@ -552,6 +556,7 @@ struct RayAccum {
     T = ex2_approx(-1.4426950408889634f * od);
   }
 #else
+  __device__ static float alpha(float x) { return -expm1f(-x); }
   __device__ void add_sample(float sig, const float* W, float tj, float dt) {
     const bool on = sig > 0.f;
     const float ods = on ? sig * dt : 0.f;
