@@ -76,10 +76,13 @@ def workload(name: str):
     raise ValueError(name)
 
 
-def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2"):
+def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world: int = 1):
     """Training step (fwd + L1/DSSIM loss + bwd + iso loss + Adam, BVH rebuilt
-    every step) on one GPU; target = render of the scene with jittered means.
-    C2 by default; C4 (3M, 1237x822) with --train-config c4."""
+    every step); target = render of the scene with jittered means.  C2 by
+    default; C4 (3M, 1237x822) with --train-config c4.  Under torchrun every
+    rank renders and back-propagates its interleaved tiles and the [N,87]
+    gradient is NCCL all-reduced (train.Trainer); the step time is the max
+    over ranks."""
     import torch
 
     from paper_2509_07782_b200.train import Trainer
@@ -102,13 +105,28 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2"):
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = tr.step(target, want_loss=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        dist.barrier()
     e0.record(s)
     for _ in range(steps):
         tr.step(target)
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     l1 = tr.step(target, want_loss=True)
+    out = {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
+           "rays_per_step": cam_kw["width"] * cam_kw["height"], "n_gpus": world}
+    if world > 1:  # the phase breakdown below is a single-GPU, full-frame measurement
+        out["parallelism"] = f"tiles{world} + NCCL all-reduce of the [N,87] gradient"
+        return out
     # phase breakdown of one step (device events between the stages)
     from paper_2509_07782_b200.renderer import render, render_backward
 
@@ -135,9 +153,7 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2"):
               "loss_ms": ev[2].elapsed_time(ev[3]), "backward_ms": ev[3].elapsed_time(ev[4]),
               "replay_backward_ms": ev[4].elapsed_time(ev[5]),
               "forward_unlogged_ms": ev[5].elapsed_time(ev6)}
-    out = {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
-           "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
-           "rays_per_step": cam_kw["width"] * cam_kw["height"], "phases": phases}
+    out["phases"] = phases
     if tr.log is not None:
         used, ovf = tr.log.usage()
         out["march_log"] = {"used_bytes": used, "capacity_bytes": tr.log.capacity,
@@ -424,11 +440,22 @@ def main():
     e1.record(s)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps  # includes the L2 flush (conservative)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e6, "unit": "Mrays/s",
            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": H * W * 3 * 4,
            "note": "camera passed by value in the launch parameters; includes a 256 MiB L2 flush"}
 
+    train = None
+    if not args.no_train:
+        del scene
+        torch.cuda.empty_cache()
+        train = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3,
+                                 config=args.train_config, world=world)
     if rank != 0:
+        dist.destroy_process_group()
         return
     achieved = flops_frame / (ms * 1e-3) / 1e12
     traffic = None
@@ -456,11 +483,8 @@ def main():
         "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
         "step_ms": step_ms,
     }
-    if not args.no_train and world == 1:
-        del scene
-        torch.cuda.empty_cache()
-        out["train_step"] = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3,
-                                             config=args.train_config)
+    if train is not None:
+        out["train_step"] = train
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
