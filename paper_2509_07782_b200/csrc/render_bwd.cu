@@ -54,8 +54,18 @@ struct PixelGrad {
 // (~240 instructions per candidate) becomes ~45 + 1/32 of the finish.
 constexpr int RED_ROW = 36;
 constexpr int RED_ROWS_A = 37;
-constexpr int RED_ROWS_B = 49;
-constexpr int RED_FLOATS = RED_ROWS_B * RED_ROW;  // reduction rows per warp
+// half B in lobe groups of SG_GROUP (7: one pass of 49 rows; 4: two passes of
+// 28 and 21 rows, so the buffer is sized by half A and a CTA needs 15% less
+// shared memory).  Logged backward, C2 ms (profiles/time_bwd_variants.py):
+// 7 / 4 CTAs x 128 regs 13.13 (this build); 4 13.74; 4 + 5 CTAs x 96 regs
+// 15.73; 7 + 3 CTAs x 168 regs (no spills) 13.55; 5 CTAs x 96 regs 16.60;
+// 64-thread CTAs x 8 13.40.  More warps do not pay for the spills.
+#ifndef GSX_BWD_SG_GROUP
+#define GSX_BWD_SG_GROUP 7
+#endif
+constexpr int SG_GROUP = GSX_BWD_SG_GROUP;
+constexpr int RED_ROWS_B = 7 * SG_GROUP;
+constexpr int RED_FLOATS = (RED_ROWS_B > RED_ROWS_A ? RED_ROWS_B : RED_ROWS_A) * RED_ROW;
 constexpr int BAT_ROW = 33;                        // 31 values + candidate id, padded
 constexpr int BAT_FLOATS = 32 * BAT_ROW;
 constexpr int BWD_WARP_FLOATS = RED_FLOATS + BAT_FLOATS;  // shared floats per warp
@@ -279,31 +289,35 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
   // float4 of lobe data out of registers); the lobe value is recomputed
   const float4* ap = sv.app + GSX_APP_F4 * p;
 #pragma unroll 1
-  for (int l = 0; l < 7; ++l) {
-    const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
-    const float cs2 = fmaf(ax.x, r.df[0], fmaf(ax.y, r.df[1], ax.z * r.df[2]));
-    const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
-    const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
-    const float f = lb * ax.w * ga;
-    float* c = col + 7 * l * RED_ROW;
-    c[0] = f * r.df[0];
-    c[RED_ROW] = f * r.df[1];
-    c[2 * RED_ROW] = f * r.df[2];
-    c[3 * RED_ROW] = lb * (cs2 - 1.f) * ga;
-    c[4 * RED_ROW] = lb * gpc[0];
-    c[5 * RED_ROW] = lb * gpc[1];
-    c[6 * RED_ROW] = lb * gpc[2];
+  for (int l0 = 0; l0 < 7; l0 += SG_GROUP) {
+    const int nl = min(SG_GROUP, 7 - l0);
+#pragma unroll 1
+    for (int l = l0; l < l0 + nl; ++l) {
+      const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
+      const float cs2 = fmaf(ax.x, r.df[0], fmaf(ax.y, r.df[1], ax.z * r.df[2]));
+      const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
+      const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
+      const float f = lb * ax.w * ga;
+      float* c = col + 7 * (l - l0) * RED_ROW;
+      c[0] = f * r.df[0];
+      c[RED_ROW] = f * r.df[1];
+      c[2 * RED_ROW] = f * r.df[2];
+      c[3 * RED_ROW] = lb * (cs2 - 1.f) * ga;
+      c[4 * RED_ROW] = lb * gpc[0];
+      c[5 * RED_ROW] = lb * gpc[1];
+      c[6 * RED_ROW] = lb * gpc[2];
+    }
+    __syncwarp();
+    for (int row = lane; row < 7 * nl; row += 32) {
+      const float sum = row_sum(gb.red, row);
+      const int l = l0 + row / 7, k = row % 7;
+      if (k < 3)
+        brow[10 + 3 * l + k] = sum;
+      else if (sum != 0.f)
+        atomicAdd(gdst + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)), sum);
+    }
+    __syncwarp();
   }
-  __syncwarp();
-  for (int row = lane; row < RED_ROWS_B; row += 32) {
-    const float sum = row_sum(gb.red, row);
-    const int l = row / 7, k = row - 7 * l;
-    if (k < 3)
-      brow[10 + 3 * l + k] = sum;
-    else if (sum != 0.f)
-      atomicAdd(gdst + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)), sum);
-  }
-  __syncwarp();
   if (++gb.n == 32) grad_batch_flush(sv, gb, grad);
 }
 
