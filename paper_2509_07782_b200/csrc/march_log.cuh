@@ -144,8 +144,20 @@ __device__ inline void log_list(int32_t* dst, const int32_t* list, int count) {
   for (int i = threadIdx.x & 31; i < count; i += 32) __stcs(dst + i, list[i]);
 }
 
+// The record writers run once per warp iteration inside the march loop; kept
+// out of line (GSX_LOG_OOL) they stay out of the hot loop's instruction
+// footprint, and only the per-lane sample-sum stores remain inline.
+#ifndef GSX_LOG_OOL
+#define GSX_LOG_OOL 0
+#endif
+#if GSX_LOG_OOL
+#define GSX_LOG_ATTR __noinline__
+#else
+#define GSX_LOG_ATTR inline
+#endif
+
 // kind 1: a full shared-list chunk of a long candidate stream
-__device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int count) {
+__device__ GSX_LOG_ATTR void log_list_chunk(LogWriter& w, const int32_t* list, int count) {
   if (!w.base) return;
   const long long off = log_alloc(w, 128 + log_round128(4LL * count));
   if (off < 0) return;
@@ -153,26 +165,42 @@ __device__ inline void log_list_chunk(LogWriter& w, const int32_t* list, int cou
   log_list((int32_t*)(w.base + off + 128), list, count);
 }
 
+// kind 0 without the sample sums: allocates the record, writes its header,
+// the lane block (tb, dt, mc) and the list; returns the lane's first
+// sample-sum slot (nullptr for lanes without samples or on overflow) and the
+// warp-uniform stride nact / row count mmax of the sample-sum array.
+__device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list, int count,
+                                              double tb, double dt, int mc, int& nact_out,
+                                              int& mmax_out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
+  const int nact = __popc(act);
+  const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
+  nact_out = nact;
+  mmax_out = 0;
+  const LogLayout L(nact, mmax, count);
+  const long long off = log_alloc(w, L.bytes);
+  if (off < 0) return nullptr;
+  mmax_out = mmax;
+  log_header(w, off, count, 0, mmax, act);
+  char* body = w.base + off + 128;
+  log_list((int32_t*)(body + L.list), list, count);
+  if (mc <= 0) return nullptr;
+  const int slot = __popc(act & ((1u << lane) - 1u));
+  __stcs((double*)body + slot, tb);
+  __stcs((double*)(body + L.dt) + slot, dt);
+  __stcs((int*)(body + L.mc) + slot, mc);
+  return (float4*)(body + L.smp) + slot;
+}
+
 // kind 0: the active lanes' block, their per-sample sums, the last list chunk
 __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, double tb,
                                 double dt, int mc, const float (&sig)[16],
                                 const float (&W)[16][3]) {
   if (!w.base) return;
-  const int lane = threadIdx.x & 31;
-  const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
-  const int nact = __popc(act);
-  const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
-  const LogLayout L(nact, mmax, count);
-  const long long off = log_alloc(w, L.bytes);
-  if (off < 0) return;
-  log_header(w, off, count, 0, mmax, act);
-  char* body = w.base + off + 128;
-  if (mc > 0) {
-    const int slot = __popc(act & ((1u << lane) - 1u));
-    __stcs((double*)body + slot, tb);
-    __stcs((double*)(body + L.dt) + slot, dt);
-    __stcs((int*)(body + L.mc) + slot, mc);
-    float4* smp = (float4*)(body + L.smp) + slot;
+  int nact, mmax;
+  float4* smp = log_full_head(w, list, count, tb, dt, mc, nact, mmax);
+  if (smp) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (j < mmax)
@@ -181,7 +209,6 @@ __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, do
                       : make_float4(0.f, 0.f, 0.f, 0.f));
     }
   }
-  log_list((int32_t*)(body + L.list), list, count);
 }
 
 // end of the warp: publish its chain head and whether it is complete

@@ -494,6 +494,9 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
 // record: replay the compositing from the saved sums to form the adjoints,
 // then pass 2 over the saved candidate stream.  Warp layout = the forward's
 // (FWD_THREADS-thread CTAs, Z-order 8x4 blocks), so the records line up.
+#ifndef GSX_BWD_LDGRP
+#define GSX_BWD_LDGRP 1
+#endif
 #ifndef GSX_BWDL_THREADS
 #define GSX_BWDL_THREADS 128
 #endif
@@ -550,6 +553,29 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     const int nact = __popc(act);
     const float dtf = (float)dt;
     float wos[16], hh[16];
+#if GSX_BWD_LDGRP
+    // the saved sums in groups of 4 samples: the 4 loads issue before the
+    // first adjoint needs one (the adjoint chain is sequential)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      float4 v[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * g + jj;
+        wos[j] = hh[j] = 0.f;
+        v[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < mmax && j < mc) v[jj] = __ldcs(smp + (long long)j * nact);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * g + jj;
+        if (j < mmax && j < mc) {
+          const float Wj[3] = {v[jj].y, v[jj].z, v[jj].w};
+          sample_adjoint(acc, pg, v[jj].x, Wj, (float)(tb + (double)j * dt), dtf, wos[j], hh[j]);
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       wos[j] = hh[j] = 0.f;
@@ -559,6 +585,7 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
         sample_adjoint(acc, pg, v.x, Wj, (float)(tb + (double)j * dt), dtf, wos[j], hh[j]);
       }
     }
+#endif
     const SegBase base = seg_base(r, tb);
     const bool want = mc > 0;
     // pass 2 over the record chain start..off

@@ -138,6 +138,9 @@ __device__ inline void sh_basis_f(const float* d, float* Y) {
 struct LdgLoad {
   __device__ float4 operator()(const float4* p) const { return __ldg(p); }
 };
+struct PlainLoad {  // ordinary load (shared memory when the pointer is known to be)
+  __device__ float4 operator()(const float4* p) const { return *p; }
+};
 struct SmemLoad {
   __device__ float4 operator()(const float4* p) const {
     float4 v;
