@@ -596,9 +596,12 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
       for (int i0 = 0; i0 < count; i0 += 32) {
         const int ent = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
         const int nb = min(32, count - i0);
-        for (int k = 0; k < nb; ++k)
+        // (an L1 prefetch of entry k + 1 / k + 2's geometry and appearance
+        // measured slower: 13.15 vs 12.58 ms on C2)
+        for (int k = 0; k < nb; ++k) {
           grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), want, mc, base, dtf, Y, pg,
                          wos, hh, gb, grad);
+        }
       }
       if (o == off) break;
       o = ho->next;

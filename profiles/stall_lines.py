@@ -9,8 +9,10 @@ import csv, io, subprocess, sys
 rep = sys.argv[1]
 col = sys.argv[2] if len(sys.argv) > 2 else "Warp Stall Sampling (All Samples)"
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+import os
+kf = ["--kernel-name", os.environ["KERNEL"]] if os.environ.get("KERNEL") else []  # e.g. regex:k_render_camera
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",
-                      "--print-source", "cuda,sass"],
+                      "--print-source", "cuda,sass", *kf],
                      capture_output=True, text=True).stdout
 fname, h, data = "?", None, []
 for r in csv.reader(io.StringIO(out)):
