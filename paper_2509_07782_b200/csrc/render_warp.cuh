@@ -30,8 +30,17 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GSX_SYNC_BWD
 #define GSX_SYNC_BWD 0.5f
 #endif
-constexpr int LCAP = 256;    // warp candidate list (shared memory)
-constexpr int WSTACK = 256;  // warp traversal stack (shared memory)
+// (shrinking the per-warp shared block -- list / stack 192, the SH basis out
+// of shared memory -- to enlarge L1 for the spilled per-lane state measured
+// within noise: C3 29.5-29.6 ms for all four, profiles/r04_smem_size_variants.txt)
+#ifndef GSX_LCAP
+#define GSX_LCAP 256
+#endif
+#ifndef GSX_WSTACK
+#define GSX_WSTACK 256
+#endif
+constexpr int LCAP = GSX_LCAP;      // warp candidate list (shared memory)
+constexpr int WSTACK = GSX_WSTACK;  // warp traversal stack (shared memory)
 
 // Optional per-phase warp-time accounting (experiment builds only:
 // nvcc -DGSX_PHASE_PROF); compiled out of the product library.
