@@ -149,15 +149,22 @@ __global__ void k_bounds_partial(SceneView v, int64_t n) {
     for (int k = 0; k < 6; ++k) v.part[6 * blockIdx.x + k] = sh[k][0];
 }
 
+// one warp: lanes stride over the partials, then a shuffle min / max tree
+// (a single serial thread took 85 us for 296 partials)
 __global__ void k_bounds_final(SceneView v, int nblocks) {
-  if (threadIdx.x != 0) return;
   double acc[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  for (int b = 0; b < nblocks; ++b)
+  for (int b = threadIdx.x; b < nblocks; b += 32)
     for (int k = 0; k < 3; ++k) {
       acc[k] = fmin(acc[k], v.part[6 * b + k]);
       acc[3 + k] = fmax(acc[3 + k], v.part[6 * b + 3 + k]);
     }
-  for (int k = 0; k < 6; ++k) v.bounds[k] = acc[k];
+  for (int o = 16; o > 0; o >>= 1)
+    for (int k = 0; k < 3; ++k) {
+      acc[k] = fmin(acc[k], __shfl_xor_sync(0xffffffffu, acc[k], o));
+      acc[3 + k] = fmax(acc[3 + k], __shfl_xor_sync(0xffffffffu, acc[3 + k], o));
+    }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) v.bounds[k] = acc[k];
 }
 
 }  // namespace
