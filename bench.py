@@ -314,9 +314,9 @@ def main():
         v = cb["value"]
         print(json.dumps({
             "metric": METRIC, "value": v, "unit": "Mrays/s", "impl": "reference",
-            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "host_only": True, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * H * W / (v * 1e6), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config, "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind",
                                                                   "sample")},
             "e2e": {"value": v, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
