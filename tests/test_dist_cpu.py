@@ -85,9 +85,12 @@ def _free_port():
 def test_tiles_partition():
     from paper_2509_07782_b200.train import tiles_of_rank
 
-    for world in (1, 2, 3, 8):
-        seen = sorted(t for r in range(world) for t in tiles_of_rank(8160, r, world))
-        assert seen == list(range(8160))
+    for n_tiles in (1, 7, 35, 100, 4029, 8160):
+        for world in (1, 2, 3, 5, 8):
+            per = [tiles_of_rank(n_tiles, r, world) for r in range(world)]
+            seen = sorted(t for p in per for t in p)
+            assert seen == list(range(n_tiles)), (n_tiles, world)
+            assert all(list(p) == sorted(p) for p in per)
 
 
 @pytest.mark.parametrize("world", [2])

@@ -333,6 +333,61 @@ def test_ess_and_tiles_invariance(G):
     assert np.array_equal(rgb.cpu().numpy(), full)
 
 
+def test_rank_shards_cover_frame(G):
+    """bench/train tile sharding (rank r of N: tile_begin=r, tile_stride=N):
+    each rank writes exactly the tiles train.tiles_of_rank names, the union
+    is the full frame bit for bit; ragged 100x75 image (7x5 tiles)."""
+    import torch
+
+    from paper_2509_07782_b200.train import tiles_of_rank
+
+    c1 = gscene(G, "c1")
+    cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=100, height=75)[0]
+    cfg = G.RenderConfig()
+    full = G.render(c1, cam, cfg)[0].cpu().numpy()
+    for world in (2, 3, 8):
+        union = np.full((75, 100, 3), -1.0, dtype=np.float32)
+        for r in range(world):
+            rgb = torch.full((75, 100, 3), -1.0, device="cuda")
+            G.render(c1, cam, cfg, tile_begin=r, tile_stride=world, rgb=rgb)
+            got = rgb.cpu().numpy()
+            mask = np.zeros((75, 100), dtype=bool)
+            for t in tiles_of_rank(35, r, world):
+                ty, tx = divmod(t, 7)
+                mask[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16] = True
+            assert np.all(got[~mask] == -1.0), (world, r)
+            assert np.array_equal(got[mask], full[mask]), (world, r)
+            union[mask] = got[mask]
+        assert np.array_equal(union, full), world
+
+
+def test_rank_shards_backward_sum(G):
+    """Logged forward + logged backward per rank shard sum to the
+    single-launch backward (fp32 atomics: rel 1e-3 of the largest entry)."""
+    import torch
+
+    c1 = gscene(G, "c1")
+    cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=100, height=75)[0]
+    cfg = G.RenderConfig()
+    rgb, depth, trans, _ = G.render(c1, cam, cfg)
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    gC = torch.randn((75, 100, 3), generator=gen).cuda()
+    ref = G.render_backward(c1, cam, cfg, rgb, depth, trans, gC).cpu().numpy()
+    world = 3
+    acc = torch.zeros((c1.n, 87), dtype=torch.float32, device="cuda")
+    for r in range(world):
+        lg = G.MarchLog(cam, tile_begin=r, tile_stride=world)
+        o = [torch.zeros_like(x) for x in (rgb, depth, trans)]
+        G.render(c1, cam, cfg, tile_begin=r, tile_stride=world, rgb=o[0], depth=o[1],
+                 trans=o[2], log=lg)
+        G.render_backward(c1, cam, cfg, o[0], o[1], o[2], gC, grad=acc, tile_begin=r,
+                          tile_stride=world, log=lg)
+    got = acc.cpu().numpy()
+    scale = np.max(np.abs(ref))
+    assert scale > 0
+    assert np.max(np.abs(got - ref)) <= 1e-3 * scale
+
+
 def test_morton_invariance(G):
     g = golden("render_small")
     cam = camera_from(G, g, "cam16")
