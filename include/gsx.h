@@ -178,9 +178,11 @@ int gsx_closest_hit(const void* scene_arena, const void* bvh_arena, int64_t n,
                     const double* queries, int64_t m, double* t_out, void* stream);
 
 /* ---- forward render (render_image renderer.py:396-437 / march_ray :263-285)
- * Camera variant: renders the 16x16 tiles t = tile_begin + k*tile_stride
- * (k = 0,1,...) of the image (multi-GPU: rank r of G uses tile_begin=r,
- * tile_stride=G).  rgb [H,W,3] f32, depth [H,W] f32 (sum_j w_j t_j),
+ * Camera variant: renders the 16x16 tiles at tile-sequence positions
+ * tile_begin + k*tile_stride (k = 0,1,...) of the image (multi-GPU: rank r of
+ * G uses tile_begin=r, tile_stride=G).  The sequence is row-major for
+ * tile_stride 1 and visits the tile rows centre-out for tile_stride > 1
+ * (gsx_tile_at in csrc/gsx_common.cuh); every rank set is a partition.  rgb [H,W,3] f32, depth [H,W] f32 (sum_j w_j t_j),
  * trans [H,W] f32 (exp(-optical depth)); pixels outside the tile set are not
  * written.  stats (device gsx_stats) may be NULL.
  * Rays variant: rays [m,8] f64 (o, d, t_near, t_far); clip != 0 applies

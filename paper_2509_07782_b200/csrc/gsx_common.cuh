@@ -11,6 +11,29 @@
 #define GSX_STACK 96
 
 // ---------------------------------------------------------------------------
+// Tile order of camera launches (render_image's tile loop renderer.py:408-412).
+// A launch renders the tile-sequence positions s = tile_begin + k*tile_stride
+// (rank r of G: tile_begin = r, tile_stride = G).  With GSX_TILE_ORDER 1 and
+// tile_stride > 1 the sequence visits the tile rows centre-out (c, c+1, c-1, c+2, ... with
+// c = (rows-1)/2; row-major inside a row), so the CTAs dispatched first are
+// the ones whose rays cross the middle of the view, and the last wave of a
+// short per-rank launch is the image border.  Pixels do not depend on the
+// order; every rank set is still a partition.  C3 8-rank share: max over
+// ranks 5.87 vs 6.22 ms row-major; a whole-image launch (stride 1) stays
+// row-major (29.58 vs 29.71 ms centre-out; profiles/r05_cta_order_variants.txt).
+// ---------------------------------------------------------------------------
+#ifndef GSX_TILE_ORDER
+#define GSX_TILE_ORDER 1
+#endif
+__host__ __device__ inline int64_t gsx_tile_at(int64_t s, int64_t tiles_x, int64_t tiles_y,
+                                               int64_t stride) {
+  if (!GSX_TILE_ORDER || stride <= 1) return s;
+  const int64_t i = s / tiles_x, c = (tiles_y - 1) / 2, d = (i + 1) / 2;
+  const int64_t row = (i & 1) ? c + d : c - d;
+  return row * tiles_x + s % tiles_x;
+}
+
+// ---------------------------------------------------------------------------
 // Scene arena (caller-allocated, gsx_scene_arena_bytes).  N primitives in
 // storage order.  Sections are 256-byte aligned.
 //   aabb64 : double[n][6]  lo xyz, hi xyz   (scene.py:61-65, exact fp64)

@@ -222,7 +222,8 @@ constexpr int FWD_THREADS = GSX_FWD_THREADS;
 
 
 // One warp block: the 32 rays of an 8x4 Z-order pixel block.  blk numbers the
-// blocks of the launch: tile tile_begin + (blk / 8) * tile_stride, warp blk % 8
+// blocks of the launch: tile at sequence position tile_begin + (blk / 8) *
+// tile_stride (gsx_tile_at), warp blk % 8
 // of the tile (the march-log warp id).
 template <bool STATS, bool SAVE>
 __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
@@ -232,7 +233,8 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
                                   WarpSmem& sw) {
   const int64_t W = cam.width, H = cam.height;
   const int64_t tiles_x = (W + 15) / 16;
-  const int64_t tile = tile_begin + (int64_t)(blk >> 3) * tile_stride;
+  const int64_t tile = gsx_tile_at(tile_begin + (int64_t)(blk >> 3) * tile_stride, tiles_x,
+                                   (H + 15) / 16, tile_stride);
   const unsigned lane = threadIdx.x & 31;
   int mx, my;
   morton_decode8((unsigned)(blk & 7) * 32 + lane, mx, my);
@@ -258,27 +260,50 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
 
 // (Persistent warps pulling pixel blocks from a launch-wide counter measured
 // slower: C3 34.1 vs 33.9 ms -- the block loop costs registers / spills.)
-template <bool STATS, bool SAVE>
-__global__ void __launch_bounds__(FWD_THREADS, GSX_FWD_MINB)
-    k_render_camera(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
-                    int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
-                    float* trans, gsx_stats* stats, void* log, long long log_nw) {
-  __shared__ WarpSmem smem[FWD_THREADS / 32];
-  const long long blk = (long long)blockIdx.x * (FWD_THREADS / 32) + (threadIdx.x >> 5);
+// One-warp CTAs (32 per SM at the same 64-register cap) for the plain forward
+// of a whole image: a finished warp frees its slot at once instead of waiting
+// for the slowest warp of its CTA.  C3 29.1 vs 29.6 ms (128-thread CTAs); the
+// logged forward (C2 17.55 vs 17.0) and short per-rank launches (8-rank C3
+// share 6.48 vs 5.87 ms) keep FWD_THREADS (profiles/r05_cta_order_variants.txt).
+#ifndef GSX_FWD_THREADS_WHOLE
+#define GSX_FWD_THREADS_WHOLE 32
+#endif
+template <bool STATS, bool SAVE, int NT>
+__global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_camera(
+    SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
+    int64_t tile_stride, float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
+    long long log_nw) {
+  __shared__ WarpSmem smem[NT / 32];
+  const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   render_warp_block<STATS, SAVE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
                                  trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
 }
 
 // Launch k_render_camera over ntl tiles (8 warp blocks each).
+template <bool STATS, bool SAVE, int NT>
+int launch_camera_nt(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
+                     const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride,
+                     int64_t ntl, float* rgb, float* depth, float* trans, gsx_stats* stats,
+                     void* log, long long log_nw, cudaStream_t s) {
+  const long long ctas = 8 * (long long)ntl / (NT / 32);
+  k_render_camera<STATS, SAVE, NT><<<(unsigned)ctas, NT, 0, s>>>(
+      sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, stats, log, log_nw);
+  return gsx_check_launch();
+}
 template <bool STATS, bool SAVE>
 int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
                   const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride, int64_t ntl,
                   float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
                   long long log_nw, cudaStream_t s) {
-  const long long ctas = 8 * (long long)ntl / (FWD_THREADS / 32);
-  k_render_camera<STATS, SAVE><<<(unsigned)ctas, FWD_THREADS, 0, s>>>(
-      sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, stats, log, log_nw);
-  return gsx_check_launch();
+  if constexpr (!SAVE && !STATS) {
+    if (tile_stride == 1)
+      return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE>(
+          sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log, log_nw,
+          s);
+  }
+  return launch_camera_nt<STATS, SAVE, FWD_THREADS>(sv, bv, cam, cfg, tile_begin, tile_stride,
+                                                    ntl, rgb, depth, trans, stats, log, log_nw,
+                                                    s);
 }
 
 template <bool STATS>

@@ -432,7 +432,8 @@ __device__ inline bool tile_pixel_ray(const SceneView& sv, const gsx_camera& cam
                                       int threads, RayCtx& r, bool& hit, int64_t& pix) {
   const int64_t W = cam.width, H = cam.height;
   const int64_t tiles_x = (W + 15) / 16;
-  const int64_t tile = tile_begin + (int64_t)(blockIdx.x / per_tile) * tile_stride;
+  const int64_t tile = gsx_tile_at(tile_begin + (int64_t)(blockIdx.x / per_tile) * tile_stride,
+                                   tiles_x, (H + 15) / 16, tile_stride);
   int mx, my;
   morton_decode8((blockIdx.x % per_tile) * threads + threadIdx.x, mx, my);
   const int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;

@@ -34,9 +34,29 @@ LR_GROUPS = {"mean": (0, 3, 1e-4), "quat": (3, 7, 1e-3), "scale": (7, 10, 1e-4),
              "sharp": (59, 66, 1e-2), "amp": (66, 87, 2.5e-3)}
 
 
-def tiles_of_rank(n_tiles: int, rank: int, world: int) -> range:
-    """Tiles rendered by `rank`: t = rank + k*world (interleaved for load balance)."""
-    return range(rank, n_tiles, world)
+TILE_ORDER = 1  # GSX_TILE_ORDER (csrc/gsx_common.cuh)
+
+
+def tile_at(s: int, tiles_x: int, tiles_y: int, stride: int) -> int:
+    """Row-major tile id at tile-sequence position s of a launch with
+    tile_stride `stride`: for stride > 1 the tile rows run centre-out
+    (c, c+1, c-1, ...; c = (tiles_y-1)//2) -- gsx_tile_at, csrc/gsx_common.cuh."""
+    if not TILE_ORDER or stride <= 1:
+        return s
+    i, c = s // tiles_x, (tiles_y - 1) // 2
+    d = (i + 1) // 2
+    row = c + d if i & 1 else c - d
+    return row * tiles_x + s % tiles_x
+
+
+def tiles_of_rank(n_tiles: int, rank: int, world: int, tiles_x: int | None = None) -> list:
+    """Row-major tile ids rendered by `rank` (tile_begin=rank,
+    tile_stride=world): sequence positions rank + k*world (interleaved for
+    load balance), through the centre-out row order when world > 1.  tiles_x = tiles per
+    image row (default: n_tiles, i.e. one row)."""
+    tx = n_tiles if tiles_x is None else tiles_x
+    ty = n_tiles // tx
+    return [tile_at(s, tx, ty, world) for s in range(rank, n_tiles, world)]
 
 
 def assemble_tiles(buffers, group=None):

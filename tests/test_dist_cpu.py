@@ -85,12 +85,15 @@ def _free_port():
 def test_tiles_partition():
     from paper_2509_07782_b200.train import tiles_of_rank
 
-    for n_tiles in (1, 7, 35, 100, 4029, 8160):
+    for tx, ty in ((1, 1), (7, 1), (7, 5), (10, 10), (79, 51), (120, 68), (120, 67)):
+        n_tiles = tx * ty
         for world in (1, 2, 3, 5, 8):
-            per = [tiles_of_rank(n_tiles, r, world) for r in range(world)]
+            per = [tiles_of_rank(n_tiles, r, world, tx) for r in range(world)]
             seen = sorted(t for p in per for t in p)
-            assert seen == list(range(n_tiles)), (n_tiles, world)
-            assert all(list(p) == sorted(p) for p in per)
+            assert seen == list(range(n_tiles)), (tx, ty, world)
+    # sharded launches visit the tile rows centre-out; a whole image is row-major
+    assert tiles_of_rank(8160, 0, 2, 120)[:2] == [33 * 120, 33 * 120 + 2]
+    assert tiles_of_rank(8160, 0, 1, 120)[:2] == [0, 1]
 
 
 @pytest.mark.parametrize("world", [2])
