@@ -64,6 +64,8 @@
 #define GSX_CONE_CH 1
 #endif
 #define FWD_CONE(save) (GSX_FWD_CONE == 1 || (GSX_FWD_CONE == 2 && !(save)))
+#include <cstdlib>
+
 #include "gsx_common.cuh"
 #include "march_log.cuh"
 #include "render_warp.cuh"
@@ -225,7 +227,7 @@ constexpr int FWD_THREADS = GSX_FWD_THREADS;
 // blocks of the launch: tile at sequence position tile_begin + (blk / 8) *
 // tile_stride (gsx_tile_at), warp blk % 8
 // of the tile (the march-log warp id).
-template <bool STATS, bool SAVE>
+template <bool STATS, bool SAVE, bool CONE>
 __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
                                   const gsx_render_cfg& cfg, int64_t tile_begin,
                                   int64_t tile_stride, long long blk, float* rgb, float* depth,
@@ -246,7 +248,7 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
   RayAccum acc;
   acc.init();
   LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
-  march_forward<STATS, SAVE, FWD_CONE(SAVE)>(sv, bv, r, hit, cfg, acc, cnt, sw, lw);
+  march_forward<STATS, SAVE, CONE>(sv, bv, r, hit, cfg, acc, cnt, sw, lw);
   if (SAVE) log_finish(lw, log_nw);
   if (valid) {
     int64_t pix = py * W + px;
@@ -265,28 +267,31 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
 // for the slowest warp of its CTA.  C3 29.1 vs 29.6 ms (128-thread CTAs); the
 // logged forward (C2 17.55 vs 17.0) and short per-rank launches (8-rank C3
 // share 6.48 vs 5.87 ms) keep FWD_THREADS (profiles/r05_cta_order_variants.txt).
+#ifndef GSX_CONE_MIN_FOCAL
+#define GSX_CONE_MIN_FOCAL 1024.0
+#endif
 #ifndef GSX_FWD_THREADS_WHOLE
 #define GSX_FWD_THREADS_WHOLE 32
 #endif
-template <bool STATS, bool SAVE, int NT>
+template <bool STATS, bool SAVE, int NT, bool CONE>
 __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_camera(
     SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
     int64_t tile_stride, float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
     long long log_nw) {
   __shared__ WarpSmem smem[NT / 32];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
-  render_warp_block<STATS, SAVE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
+  render_warp_block<STATS, SAVE, CONE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
                                  trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
 }
 
 // Launch k_render_camera over ntl tiles (8 warp blocks each).
-template <bool STATS, bool SAVE, int NT>
+template <bool STATS, bool SAVE, int NT, bool CONE = FWD_CONE(SAVE)>
 int launch_camera_nt(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
                      const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride,
                      int64_t ntl, float* rgb, float* depth, float* trans, gsx_stats* stats,
                      void* log, long long log_nw, cudaStream_t s) {
   const long long ctas = 8 * (long long)ntl / (NT / 32);
-  k_render_camera<STATS, SAVE, NT><<<(unsigned)ctas, NT, 0, s>>>(
+  k_render_camera<STATS, SAVE, NT, CONE><<<(unsigned)ctas, NT, 0, s>>>(
       sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, stats, log, log_nw);
   return gsx_check_launch();
 }
@@ -295,6 +300,25 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
                   const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride, int64_t ntl,
                   float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
                   long long log_nw, cudaStream_t s) {
+  if constexpr (!SAVE && !STATS && FWD_CONE(false)) {
+    // wide pixels (focal < GSX_CONE_MIN_FOCAL px): a warp's 8x4-pixel cone
+    // lists many entries its rays miss, and the per-lane packet traversal
+    // wins (480x270, f = 576, 1M / 3M / 5M: 10.4 / 17.4 / 22.7 vs 11.9 /
+    // 19.7 / 25.6 ms; C2 f = 1111 equal; C3 f = 2304: cone 31.2 vs 34.7)
+    // GSX_CONE_MIN_FOCAL in the environment overrides the threshold (tests
+    // force either traversal with it); read per launch, no library state
+    const char* env = getenv("GSX_CONE_MIN_FOCAL");
+    const double min_focal = env ? atof(env) : GSX_CONE_MIN_FOCAL;
+    if (cam.focal < min_focal) {
+      if (tile_stride == 1)
+        return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE, false>(
+            sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log,
+            log_nw, s);
+      return launch_camera_nt<STATS, SAVE, FWD_THREADS, false>(
+          sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log, log_nw,
+          s);
+    }
+  }
   if constexpr (!SAVE && !STATS) {
     if (tile_stride == 1)
       return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE>(

@@ -70,3 +70,31 @@ def test_cone_far_background_vs_oracle():
                                                       O.OCfg.make(mode=mode))
         assert np.max(np.abs(rgb - R)) < 1e-4
         assert np.max(np.abs(trans - T)) < 1e-4
+
+
+@pytest.mark.parametrize("min_focal", ["0", "1e30"])
+def test_plain_forward_traversal_choice(monkeypatch, min_focal):
+    """The plain whole-image / sharded forward picks the packet cone for
+    focal >= GSX_CONE_MIN_FOCAL and the per-lane packet traversal below it;
+    both equal the oracle (forced here through the environment override)."""
+    import torch
+
+    import paper_2509_07782_b200 as G
+
+    monkeypatch.setenv("GSX_CONE_MIN_FOCAL", min_focal)
+    rec = synth_records("ball", 3000, seed=2, anisotropy=3.0, r_max_bound=10.0,
+                        shell_fraction=0.3, shell_radius=(10.0, 50.0))
+    scene = G.Scene.from_records(rec)
+    G.reorder_by_morton(scene)
+    cam = G.orbit_cameras(1, radius=3.5, focal=1.2 * 40, width=40, height=24)[0]
+    cfg = G.RenderConfig(mode="adaptive")
+    rays = O.camera_rays(cam.center, cam.quat, cam.focal, cam.width, cam.height)
+    R, T, D, _ = O.OracleScene(rec, 0.01).render(rays, cam.height, cam.width,
+                                                  O.OCfg.make(mode="adaptive"))
+    rgb, depth, trans, _ = G.render(scene, cam, cfg)
+    assert np.max(np.abs(rgb.cpu().numpy() - R)) < 1e-4
+    assert np.max(np.abs(trans.cpu().numpy() - T)) < 1e-4
+    out = torch.zeros_like(rgb)
+    for r in range(2):
+        G.render(scene, cam, cfg, tile_begin=r, tile_stride=2, rgb=out)
+    assert np.max(np.abs(out.cpu().numpy() - R)) < 1e-4
