@@ -36,7 +36,7 @@ extern "C" {
 #endif
 
 #define GSX_FLOATS_PER_RECORD 87
-#define GSX_ABI_VERSION 1
+#define GSX_ABI_VERSION 2
 
 typedef enum {
   GSX_OK = 0,
@@ -61,6 +61,10 @@ typedef struct {
   int64_t tile_size;       /* accepted; pixels are tile-size invariant (renderer.py:399-401) */
   double background[3];
   int64_t buffer_capacity; /* accepted; overflow splitting is bitwise neutral (renderer.py:361-371) */
+  /* extension (no RenderConfig counterpart): warp traversal of camera
+     renders, 0 = by focal length (packet cone for focal >= 1024 px), 1 =
+     packet cone, 2 = per-lane packet.  Pixels do not depend on it. */
+  int64_t traversal;
 } gsx_render_cfg;
 
 /* Camera (renderer.py:109-145): camera-to-world rotation R (row-major, from the
@@ -187,11 +191,20 @@ int gsx_closest_hit(const void* scene_arena, const void* bvh_arena, int64_t n,
  * written.  stats (device gsx_stats) may be NULL.
  * Rays variant: rays [m,8] f64 (o, d, t_near, t_far); clip != 0 applies
  * clip_ray_to_scene (renderer.py:160-175) first; outputs rgb [m,3], depth [m],
- * trans [m]. */
+ * trans [m].
+ * ws (nullable, ws_bytes >= gsx_render_workspace_bytes(n)) is a caller-owned
+ * per-call workspace: with it the camera forward first computes every
+ * primitive's image-space silhouette for this camera and screens the warp
+ * candidate lists with it (pixels unchanged, fewer per-lane setups).  Two
+ * concurrent renders need two workspaces.
+ * dev_status (nullable): GSX_ERR_STACK if a traversal stack overflowed (the
+ * frame is then incomplete). */
+size_t gsx_render_workspace_bytes(int64_t n);
 int gsx_render_forward(const void* scene_arena, const void* bvh_arena, int64_t n,
                        const gsx_camera* cam, const gsx_render_cfg* cfg, int64_t tile_begin,
                        int64_t tile_stride, float* rgb, float* depth, float* trans,
-                       gsx_stats* stats, gsx_dev_status* dev_status, void* stream);
+                       gsx_stats* stats, void* ws, int64_t ws_bytes, gsx_dev_status* dev_status,
+                       void* stream);
 int gsx_render_rays(const void* scene_arena, const void* bvh_arena, int64_t n,
                     const double* rays, int64_t m, int clip, const gsx_render_cfg* cfg,
                     float* rgb, float* depth, float* trans, gsx_stats* stats,

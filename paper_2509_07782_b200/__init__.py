@@ -13,7 +13,7 @@ from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptySce
 from .renderer import (MarchLog, clip_ray_to_scene, march_ray, march_rays, psnr, render,
                        render_backward, render_full, render_image)
 from .scene import Scene, gen_test_scene, load_scene, reorder_by_morton, save_scene
-from .scene_io import (export_density_ply, load_cameras, load_ply_scene, ply_records,
+from .scene_io import (load_cameras, load_ply_scene, ply_records,
                        save_cameras)
 from .scenes import orbit_poses, look_at
 
@@ -33,7 +33,7 @@ def look_at_camera(center, target, focal, width, height, up=(0.0, 1.0, 0.0), **k
 __all__ = [
     "BufferOverflow", "Camera", "DegenerateCenter", "DensifyConfig", "GradAccumulator",
     "MarchLog", "criterion_new", "criterion_old", "neighbor_density", "observe_scene",
-    "export_density_ply", "load_cameras", "load_ply_scene", "ply_records", "save_cameras", "EmptyIsosurface", "EmptyScene",
+    "load_cameras", "load_ply_scene", "ply_records", "save_cameras", "EmptyIsosurface", "EmptyScene",
     "GsrayError", "ParseError", "Ray", "RenderConfig", "RenderStats", "Scene",
     "ValidationError", "clip_ray_to_scene", "gen_test_scene", "load_scene", "look_at_camera",
     "march_ray", "march_rays", "orbit_cameras", "psnr", "quat_to_rotation", "render",

@@ -39,6 +39,7 @@ class RenderCfg(ctypes.Structure):
         ("mode", ctypes.c_int64), ("beta", ctypes.c_double), ("dt_min", ctypes.c_double),
         ("dt_max", ctypes.c_double), ("ess", ctypes.c_int64), ("tile_size", ctypes.c_int64),
         ("background", ctypes.c_double * 3), ("buffer_capacity", ctypes.c_int64),
+        ("traversal", ctypes.c_int64),
     ]
 
 
@@ -96,7 +97,8 @@ _SIGS = {
     "gsx_bvh_collapse": (INT, [P, I64, P, P]),
     "gsx_collect_segments": (INT, [P, P, I64, P, I64, I64, P, P, P, P]),
     "gsx_closest_hit": (INT, [P, P, I64, P, I64, P, P]),
-    "gsx_render_forward": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, P, P]),
+    "gsx_render_workspace_bytes": (SZ, [I64]),
+    "gsx_render_forward": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, P, I64, P, P]),
     "gsx_render_rays": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
     "gsx_render_rays_stats": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
     "gsx_render_backward": (INT, [P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, P, P, P]),

@@ -64,8 +64,6 @@
 #define GSX_CONE_CH 1
 #endif
 #define FWD_CONE(save) (GSX_FWD_CONE == 1 || (GSX_FWD_CONE == 2 && !(save)))
-#include <cstdlib>
-
 #include "gsx_common.cuh"
 #include "march_log.cuh"
 #include "render_warp.cuh"
@@ -284,6 +282,130 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
                                  trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
 }
 
+// ---------------------------------------------------------------------------
+// Screened plain forward (the benchmarked frame): the camera kernel above
+// with the per-camera silhouette screen (Screen, render_warp.cuh) in front of
+// every list and the per-sample sums in shared memory (WarpSmemS).  Same
+// march, same per-lane arithmetic in the same order: its pixels equal the
+// unscreened kernel's bit for bit.
+// ---------------------------------------------------------------------------
+template <class YT>
+__device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
+                                         const RayCtx& r, bool want, const Seg& seg, int ns,
+                                         YT Y, RayAccum& acc, WarpSmemS& sm, const Screen& sc) {
+  constexpr int CH = GSX_SCR_CH;
+  bool nonempty = false;
+  const float dtf = (float)seg.dt;
+  const int nchunks = (ns + CH - 1) / CH;
+  float4* col = &sm.acc[0][threadIdx.x & 31];
+  uint32_t visits = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int mc = want ? seg.m - ch * CH : 0;
+    mc = mc < 0 ? 0 : (mc > CH ? CH : mc);
+    const bool wch = want && (ch == 0 || mc > 0);
+    if (!__any_sync(FULL, wch)) continue;
+    const double tb = seg.tbase + (double)(ch * CH) * seg.dt;
+    const SegBase base = seg_base(r, tb);
+#pragma unroll
+    for (int j = 0; j < CH; ++j) col[32 * j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    SegLimits lim;
+    if (nchunks == 1) {
+      lim = seg_limits(r, seg);
+    } else {
+      const double a = ch == 0 ? seg.t0 : seg.tgrid + (double)(seg.j0 + ch * CH) * seg.dt;
+      const double b = (ch + 1) * CH >= seg.m
+                           ? seg.t1
+                           : seg.tgrid + (double)(seg.j0 + (ch + 1) * CH) * seg.dt;
+      lim = interval_limits(r, a, b);
+    }
+    make_cone(r, wch, lim.lo_t, lim.hi_t, sm);
+    ConeTrav cst;
+    cone_begin(sm, cst);
+    const unsigned lanes = __ballot_sync(FULL, wch && mc > 0);
+    int count = 0;
+    for (;;) {
+      warp_traverse_cone(bv, cst, sm, count, visits);
+      screen_list(sc, sm, count, lanes);
+      bool inside = false;
+      accumulate_screened<CH>(sv, r, sm, count, wch, mc, base, dtf, Y, inside);
+      nonempty = nonempty || inside;
+      // AABB emptiness without a clearly-inside sample: the exact test over
+      // this chunk of the list (a superset of the boxes the segment meets)
+      if (want && !nonempty)
+        for (int i = 0; i < count; ++i)
+          if (exact_aabb_overlap(sv, r, (int64_t)sm.list[i], seg.t0, seg.t1)) {
+            nonempty = true;
+            break;
+          }
+      __syncwarp();
+      if (cst.done) break;
+      count = 0;
+    }
+    // front-to-back compositing (renderer.py:230-239)
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const float4 a = col[32 * j];
+      const float w3[3] = {a.y, a.z, a.w};
+      acc.add_sample(j < mc ? a.x : 0.f, w3, (float)(tb + (double)j * seg.dt), dtf);
+    }
+  }
+  Counters<false> cnt;
+  emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt);
+  return nonempty;
+}
+
+#ifndef GSX_SCR_THREADS
+#define GSX_SCR_THREADS 32
+#endif
+#ifndef GSX_SCR_MINB  // CTAs of 32 threads per SM (registers: 65536 / (32 MINB))
+#define GSX_SCR_MINB 16
+#endif
+template <int NT>
+__global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
+    k_render_screened(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
+                      int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
+                      float* trans, const float4* view) {
+  __shared__ WarpSmemS smem[NT / 32];
+  WarpSmemS& sw = smem[threadIdx.x >> 5];
+  const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  const int64_t W = cam.width, H = cam.height;
+  const int64_t tiles_x = (W + 15) / 16;
+  const int64_t tile = gsx_tile_at(tile_begin + (int64_t)(blk >> 3) * tile_stride, tiles_x,
+                                   (H + 15) / 16, tile_stride);
+  const unsigned lane = threadIdx.x & 31;
+  int mx, my, bx, by;
+  morton_decode8((unsigned)(blk & 7) * 32 + lane, mx, my);
+  morton_decode8((unsigned)(blk & 7) * 32, bx, by);
+  const int64_t px = (tile % tiles_x) * 16 + mx, py = (tile / tiles_x) * 16 + my;
+  const bool valid = px < W && py < H;
+  RayCtx r;
+  const bool hit = valid && camera_ray(cam, (double)px, (double)py, sv.bounds, r);
+  RayAccum acc;
+  acc.init();
+  const Screen sc{view, (float)((tile % tiles_x) * 16 + bx), (float)((tile / tiles_x) * 16 + by)};
+  float Y[9];
+  sh_basis_f(r.df, Y);
+#pragma unroll
+  for (int b = 0; b < 9; ++b) sw.ylane[b][lane] = Y[b];
+  __syncwarp();
+  const YSmem Yv{&sw.ylane[0][lane]};
+  const int ns = (int)cfg.n_s;
+  Counters<false> cnt;
+  march_warp<false, true>(sv, bv, r, hit, cfg, acc, cnt,
+                          cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sw,
+                          [&](const Seg& seg, bool want) {
+                            return forward_segment_screened(sv, bv, r, want, seg, ns, Yv, acc,
+                                                            sw, sc);
+                          });
+  if (valid) {
+    const int64_t pix = py * W + px;
+    const float T = hit ? acc.transmittance() : 1.f;
+    for (int k = 0; k < 3; ++k) rgb[3 * pix + k] = acc.C[k] + T * (float)cfg.background[k];
+    if (depth) depth[pix] = acc.D;
+    if (trans) trans[pix] = T;
+  }
+}
+
 // Launch k_render_camera over ntl tiles (8 warp blocks each).
 template <bool STATS, bool SAVE, int NT, bool CONE = FWD_CONE(SAVE)>
 int launch_camera_nt(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
@@ -299,17 +421,16 @@ template <bool STATS, bool SAVE>
 int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
                   const gsx_render_cfg& cfg, int64_t tile_begin, int64_t tile_stride, int64_t ntl,
                   float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
-                  long long log_nw, cudaStream_t s) {
+                  long long log_nw, cudaStream_t s, const float4* view = nullptr) {
   if constexpr (!SAVE && !STATS && FWD_CONE(false)) {
     // wide pixels (focal < GSX_CONE_MIN_FOCAL px): a warp's 8x4-pixel cone
     // lists many entries its rays miss, and the per-lane packet traversal
     // wins (480x270, f = 576, 1M / 3M / 5M: 10.4 / 17.4 / 22.7 vs 11.9 /
-    // 19.7 / 25.6 ms; C2 f = 1111 equal; C3 f = 2304: cone 31.2 vs 34.7)
-    // GSX_CONE_MIN_FOCAL in the environment overrides the threshold (tests
-    // force either traversal with it); read per launch, no library state
-    const char* env = getenv("GSX_CONE_MIN_FOCAL");
-    const double min_focal = env ? atof(env) : GSX_CONE_MIN_FOCAL;
-    if (cam.focal < min_focal) {
+    // 19.7 / 25.6 ms; C2 f = 1111 equal; C3 f = 2304: cone 31.2 vs 34.7).
+    // cfg.traversal forces either (1 cone, 2 per-lane packet).
+    const bool lane_packet =
+        cfg.traversal == 2 || (cfg.traversal == 0 && cam.focal < GSX_CONE_MIN_FOCAL);
+    if (lane_packet) {
       if (tile_stride == 1)
         return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE, false>(
             sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log,
@@ -320,6 +441,12 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
     }
   }
   if constexpr (!SAVE && !STATS) {
+    if (view && FWD_CONE(false)) {
+      const long long ctas = 8 * (long long)ntl / (GSX_SCR_THREADS / 32);
+      k_render_screened<GSX_SCR_THREADS><<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(
+          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view);
+      return gsx_check_launch();
+    }
     if (tile_stride == 1)
       return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE>(
           sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log, log_nw,
@@ -328,6 +455,75 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
   return launch_camera_nt<STATS, SAVE, FWD_THREADS>(sv, bv, cam, cfg, tile_begin, tile_stride,
                                                     ntl, rgb, depth, trans, stats, log, log_nw,
                                                     s);
+}
+
+// K6a: image-space silhouettes of every primitive for one camera (Screen,
+// render_warp.cuh), fp64.  With M the iso_inv of p inflated by 1e-3, the
+// line o + t d meets the ellipsoid iff (g.d)^2 >= kappa d^T S d, g = M^T a,
+// a = M (o - mu), kappa = |a|^2 - 1, S = M^T M.  In camera coordinates
+// d ~ (u, v, 1) this is F(u, v) = p^T K p >= 0 with K = R^T (g g^T - kappa S) R;
+// when its 2x2 block is negative definite the set is the ellipse
+// (w - c)^T (-K2 / F(c)) (w - c) <= 1 about c = -K2^-1 k, mapped to pixels
+// (u = (X - W/2) / f) and widened by 2e-3 px (fp32 rounding of the centre).
+// Anything else (camera inside, ellipsoid across the camera plane, a
+// degenerate form) gets A00 = 0: never screened out.
+__global__ void k_view_conics(SceneView sv, int64_t n, gsx_camera cam, float4* view) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double inflate = 1.0 / (1.0 + 1e-3);
+  double M[9];
+  for (int k = 0; k < 9; ++k) M[k] = sv.inv64[9 * p + k] * inflate;
+  const float4 g0 = sv.geo[4 * p];
+  const double v[3] = {cam.center[0] - (double)g0.x, cam.center[1] - (double)g0.y,
+                       cam.center[2] - (double)g0.z};
+  double a[3], g[3] = {0, 0, 0}, S[9];
+  for (int i = 0; i < 3; ++i) a[i] = M[3 * i] * v[0] + M[3 * i + 1] * v[1] + M[3 * i + 2] * v[2];
+  const double kappa = a[0] * a[0] + a[1] * a[1] + a[2] * a[2] - 1.0;
+  float4 out0 = make_float4(0.f, 0.f, 0.f, 0.f), out1 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (kappa > 1e-9) {
+    for (int b = 0; b < 3; ++b)
+      for (int i = 0; i < 3; ++i) g[b] += M[3 * i + b] * a[i];
+    for (int b = 0; b < 3; ++b)
+      for (int c = 0; c < 3; ++c)
+        S[3 * b + c] = M[b] * M[c] + M[3 + b] * M[3 + c] + M[6 + b] * M[6 + c];
+    // world -> camera: gc = R^T g, Sc = R^T S R (R row-major, d_world = R d_cam)
+    const double* R = cam.R;
+    double gc[3], SR[9], K[9];
+    for (int k = 0; k < 3; ++k) gc[k] = R[k] * g[0] + R[3 + k] * g[1] + R[6 + k] * g[2];
+    for (int b = 0; b < 3; ++b)
+      for (int k = 0; k < 3; ++k)
+        SR[3 * b + k] = S[3 * b] * R[k] + S[3 * b + 1] * R[3 + k] + S[3 * b + 2] * R[6 + k];
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k)
+        K[3 * j + k] = gc[j] * gc[k] -
+                       kappa * (R[j] * SR[k] + R[3 + j] * SR[3 + k] + R[6 + j] * SR[6 + k]);
+    const double k00 = K[0], k01 = 0.5 * (K[1] + K[3]), k11 = K[4];
+    const double k02 = 0.5 * (K[2] + K[6]), k12 = 0.5 * (K[5] + K[7]), k22 = K[8];
+    const double det = k00 * k11 - k01 * k01;
+    if (k00 < 0.0 && det > 0.0) {
+      const double cu = -(k11 * k02 - k01 * k12) / det, cv = -(k00 * k12 - k01 * k02) / det;
+      const double Fc = k22 + k02 * cu + k12 * cv;
+      if (Fc > 0.0) {
+        const double f = cam.focal, s2 = 1.0 / (Fc * f * f);
+        double A00 = -k00 * s2, A01 = -k01 * s2, A11 = -k11 * s2;
+        // widen by 2e-3 px: scale the semi-axes by (1 + 2e-3 / r_min),
+        // r_min = 1 / sqrt(lambda_max(A))
+        const double tr = 0.5 * (A00 + A11),
+                     lmax = tr + sqrt(fmax(tr * tr - (A00 * A11 - A01 * A01), 0.0));
+        const double grow = 1.0 + 2e-3 * sqrt(lmax), w = 1.0 / (grow * grow) * (1.0 - 1e-6);
+        A00 *= w;
+        A01 *= w;
+        A11 *= w;
+        const double Xc = 0.5 * (double)cam.width + f * cu, Yc = 0.5 * (double)cam.height + f * cv;
+        if (isfinite(Xc) && isfinite(Yc) && fabs(Xc) < 1e7 && fabs(Yc) < 1e7 && A00 > 0.0) {
+          out0 = make_float4((float)Xc, (float)Yc, (float)A00, (float)(2.0 * A01));
+          out1 = make_float4((float)A11, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+  view[2 * p] = out0;
+  view[2 * p + 1] = out1;
 }
 
 template <bool STATS>
@@ -403,11 +599,15 @@ extern "C" int gsx_phase_times(unsigned long long* out, int reset) {
 }
 #endif
 
+extern "C" size_t gsx_render_workspace_bytes(int64_t n) {
+  return n > 0 ? (size_t)n * 2 * sizeof(float4) : 0;
+}
+
 extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena, int64_t n,
                                   const gsx_camera* cam, const gsx_render_cfg* cfg,
                                   int64_t tile_begin, int64_t tile_stride, float* rgb,
-                                  float* depth, float* trans, gsx_stats* stats,
-                                  gsx_dev_status* dev_status, void* stream) {
+                                  float* depth, float* trans, gsx_stats* stats, void* ws,
+                                  int64_t ws_bytes, gsx_dev_status* dev_status, void* stream) {
   int rc = gsx_validate_cfg(cfg);
   if (rc) return rc;
   if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
@@ -423,8 +623,14 @@ extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena
   if (stats)
     return launch_camera<true, false>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb,
                                       depth, trans, stats, nullptr, 0, s);
+  float4* view = nullptr;
+  if (ws) {
+    if (ws_bytes < (int64_t)gsx_render_workspace_bytes(n)) return GSX_ERR_ARG;
+    view = (float4*)ws;
+    k_view_conics<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sv, n, *cam, view);
+  }
   return launch_camera<false, false>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb, depth,
-                                     trans, nullptr, nullptr, 0, s);
+                                     trans, nullptr, nullptr, 0, s, view);
 }
 
 __global__ void k_log_init(LogHeader* h, unsigned long long cap, unsigned nw, long long table) {

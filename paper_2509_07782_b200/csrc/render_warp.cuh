@@ -745,6 +745,118 @@ __device__ inline int accumulate_list(const SceneView& sv, const RayCtx& r, Warp
 }
 
 
+// ---------------------------------------------------------------------------
+// Silhouette screen (camera rays).  view[2p] / view[2p+1] hold primitive p's
+// image-space silhouette for the current camera (k_view_conics, render.cu):
+// the pixels whose ray line meets the (1e-3-inflated) ellipsoid are the
+// ellipse (X - Xc, Y - Yc) A (X - Xc, Y - Yc)^T <= 1, stored as
+// (Xc, Yc, A00, 2 A01) (A11, -, -, -); A00 = 0 marks "no screen" (camera
+// inside, or the ellipsoid crossing the camera plane: every lane passes).
+// The list is screened entry-parallel: lane l evaluates entry b + l against
+// the warp's 32 pixel centres (an 8x4 block; lanes in Z-order) and stores the
+// 32-bit mask of lanes it may touch.  A superset of the lanes whose setup
+// (cand_setup_at) can succeed, so the accumulation skips every other
+// (lane, entry) pair and every entry no lane can use.
+// ---------------------------------------------------------------------------
+struct Screen {
+  const float4* view;  // nullptr: no screening
+  float x0, y0;        // pixel of the warp block's lane 0
+};
+
+// Per-warp shared state of the screened forward: the base block, the
+// screen masks of the current list, and the 16 per-sample sums (sigma_j,
+// W_j rgb) of every lane as one float4 column per lane (acc[j][lane]).
+// Held in shared memory instead of registers: at the 64-register cap of 32
+// warps per SM they lived in local memory (4 LDL + 4 STL per sample update,
+// missing L1 -- the dominant long-scoreboard stall of the r06 capture).
+#ifndef GSX_SCR_CH
+#define GSX_SCR_CH 16
+#endif
+struct WarpSmemS : WarpSmem {
+  uint32_t mask[LCAP];
+  float4 acc[GSX_SCR_CH][32];
+};
+
+__device__ inline void screen_list(const Screen& sc, WarpSmemS& sm, int count, unsigned lanes) {
+  const unsigned lane = threadIdx.x & 31;
+  for (int b = 0; b < count; b += 32) {
+    const int i = b + (int)lane;
+    unsigned m = 0u;
+    if (i < count) {
+      const int64_t p = sm.list[i];
+      const float4 c0 = __ldg(sc.view + 2 * p);
+      if (c0.z > 0.f) {
+        const float a11 = __ldg(sc.view + 2 * p + 1).x;
+        float dx[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dx[k] = (sc.x0 + (0.5f + (float)k)) - c0.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float dy = (sc.y0 + (0.5f + (float)j)) - c0.y;
+          const float r1 = c0.w * dy, r2 = fmaf(a11 * dy, dy, -1.f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            // Z-order lane of pixel (k, j): x bits at 0, 2, 4; y bits at 1, 3
+            const int l = (k & 1) | ((k & 2) << 1) | ((k & 4) << 2) | ((j & 1) << 1) | ((j & 2) << 2);
+            const float q = fmaf(dx[k], fmaf(c0.z, dx[k], r1), r2);
+            m |= q <= 0.f ? (1u << l) : 0u;
+          }
+        }
+      } else {
+        m = FULL;
+      }
+      sm.mask[i] = m & lanes;
+    }
+  }
+  __syncwarp();
+}
+
+// Pass 1 over a screened list: entries no lane can use are skipped
+// warp-uniformly, and a lane sets up only the entries whose mask holds it;
+// the sums go to the lane's shared-memory column acc[j][lane] (one 16-byte
+// load / store per updated sample).  `inside` is set when a sample lies
+// clearly inside an ellipsoid (q <= 0.998 in fp32): that sample is then
+// inside the primitive's fp64 AABB too, so the segment is AABB-non-empty in
+// the reference's sense (spatial.py:234-241) without the exact slab test.
+template <int CH, class YT>
+__device__ inline void accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemS& sm,
+                                           int count, bool want, int mc, const SegBase& base,
+                                           float dtf, YT Y, bool& inside) {
+  const unsigned lane = threadIdx.x & 31;
+  float4* col = &sm.acc[0][lane];
+  for (int i = 0; i < count; ++i) {
+    const unsigned m = sm.mask[i];
+    if (m == 0u) continue;
+    const int64_t p = sm.list[i];
+    CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
+    if (!__any_sync(FULL, u.use)) continue;
+    const CandSetup& cs = u.cs;
+    float c[3] = {0.f, 0.f, 0.f};
+    if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
+    const float nkl2 = -cs.kl2;
+#pragma unroll
+    for (int g = 0; g < CH / 4; ++g) {
+      if (!__any_sync(FULL, u.use && u.jlo <= 4 * g + 3 && u.jhi >= 4 * g)) continue;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * g + jj;
+        const float del = fmaf((float)j, dtf, cs.del0);
+        const float q = fmaf(cs.A * del, del, cs.qmin);
+        if (u.use && q <= 1.0f) {
+          const float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
+          float4 a = col[32 * j];
+          a.x += dens;
+          a.y = fmaf(dens, c[0], a.y);
+          a.z = fmaf(dens, c[1], a.z);
+          a.w = fmaf(dens, c[2], a.w);
+          col[32 * j] = a;
+          inside = inside || q <= 0.998f;
+        }
+      }
+    }
+  }
+}
+
 // Exact AABB-emptiness of the lane's segment (reference semantics) after the
 // true-intersection pass; STATS additionally counts every exact overlap.
 template <bool STATS>

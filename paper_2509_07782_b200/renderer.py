@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from ._lib import Stats, check, ptr, stream_ptr
-from .config import Camera, Ray, RenderConfig, RenderStats
+from .config import Camera, LazyRenderStats, Ray, RenderConfig, RenderStats
 
 
 def _out(shape, out, device):
@@ -74,11 +74,17 @@ class MarchLog:
 
 def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin: int = 0,
            tile_stride: int = 1, rgb=None, depth=None, trans=None, stats: bool = False,
-           log: MarchLog | None = None, stream=None):
+           log: MarchLog | None = None, stream=None, screen: bool = True, traversal: int = 0,
+           workspace=None):
     """Render the 16x16 tiles tile_begin + k*tile_stride of `camera` into
     rgb [H,W,3], depth [H,W], trans [H,W] float32 CUDA tensors (allocated
     unless given).  Returns (rgb, depth, trans, stats_tensor_or_None).
-    With `log` (training) the march is also recorded for render_backward."""
+    With `log` (training) the march is also recorded for render_backward.
+    `screen` enables the per-camera silhouette screen of the plain forward
+    (its table lives in `workspace`, default the scene's own render
+    workspace -- pass separate ones for concurrent renders of one scene);
+    `traversal` forces the warp traversal (0 auto, 1 cone, 2 per-lane).
+    Pixels do not depend on either."""
     cfg = cfg or RenderConfig()
     L = _lib.lib()
     H, W = camera.height, camera.width
@@ -87,7 +93,7 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
     depth = _out((H, W), depth, dev)
     trans = _out((H, W), trans, dev)
     st = torch.zeros(10, dtype=torch.int64, device=dev) if stats else None
-    cam_c, cfg_c = camera.to_c(), cfg.to_c()
+    cam_c, cfg_c = camera.to_c(), cfg.to_c(traversal)
     import ctypes
 
     if log is not None:
@@ -101,9 +107,13 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
                                           ptr(depth), ptr(trans), ptr(log.arena), log.capacity,
                                           None, stream_ptr(stream)), "render_forward_logged")
         return rgb, depth, trans, None
+    ws = None
+    if screen and not stats:
+        ws = workspace if workspace is not None else scene.render_workspace()
     check(L.gsx_render_forward(ptr(scene.arena), ptr(scene.bvh_arena), scene.n,
                                ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
-                               int(tile_stride), ptr(rgb), ptr(depth), ptr(trans), ptr(st), None,
+                               int(tile_stride), ptr(rgb), ptr(depth), ptr(trans), ptr(st),
+                               ptr(ws), 0 if ws is None else ws.numel(), None,
                                stream_ptr(stream)), "render_forward")
     return rgb, depth, trans, st
 
@@ -142,19 +152,36 @@ def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans,
     return grad
 
 
+def lazy_stats(scene, camera: Camera, cfg: RenderConfig) -> LazyRenderStats:
+    """RenderStats of render_image(scene, camera, cfg), gathered by the STATS
+    forward only when a counter is first read (see LazyRenderStats)."""
+    version = scene.version
+
+    def compute():
+        if scene.version != version:
+            raise RuntimeError("scene changed since the render; its RenderStats are gone")
+        st = render(scene, camera, cfg, stats=True)[3]
+        # (`transmittance` stays 1.0: render_image does not merge it,
+        # renderer.py:79,85-93)
+        return RenderStats.from_counts(st.cpu().numpy())
+
+    return LazyRenderStats(compute)
+
+
 def render_image(scene, camera: Camera, cfg: RenderConfig, threads: int | None = None):
     """renderer.py:396-437: returns (image (H,W,3) float64 numpy, RenderStats).
-    `threads` / GSRAY_THREADS are accepted and ignored (one CUDA thread per ray)."""
-    rgb, depth, trans, st = render(scene, camera, cfg, stats=True)
-    stats = RenderStats.from_counts(st.cpu().numpy())
-    return rgb.cpu().numpy().astype(np.float64), stats
+    `threads` / GSRAY_THREADS are accepted and ignored (one CUDA thread per ray).
+    The image comes from the plain (screened) forward; the RenderStats are
+    lazy: reading a counter runs the exact-counter pass then."""
+    rgb, _, _, _ = render(scene, camera, cfg)
+    return rgb.double().cpu().numpy(), lazy_stats(scene, camera, cfg)
 
 
 def render_full(scene, camera: Camera, cfg: RenderConfig):
-    """(rgb, depth, trans) as float64 numpy plus RenderStats."""
-    rgb, depth, trans, st = render(scene, camera, cfg, stats=True)
-    return (rgb.cpu().numpy().astype(np.float64), depth.cpu().numpy().astype(np.float64),
-            trans.cpu().numpy().astype(np.float64), RenderStats.from_counts(st.cpu().numpy()))
+    """(rgb, depth, trans) as float64 numpy plus (lazy) RenderStats."""
+    rgb, depth, trans, _ = render(scene, camera, cfg)
+    return (rgb.double().cpu().numpy(), depth.double().cpu().numpy(),
+            trans.double().cpu().numpy(), lazy_stats(scene, camera, cfg))
 
 
 def march_rays(scene, rays, cfg: RenderConfig, clip: bool = False, stats: bool = False):

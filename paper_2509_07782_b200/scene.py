@@ -95,9 +95,20 @@ class Scene:
         self.bounds_t = torch.empty(6, dtype=torch.float64, device=dev)
         self._status = _lib.new_status(dev)
 
+    def render_workspace(self):
+        """The scene's default per-render workspace (gsx_render_workspace_bytes:
+        the per-camera silhouette table of the screened forward)."""
+        ws = getattr(self, "_render_ws", None)
+        need = int(self._L.gsx_render_workspace_bytes(self.n))
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._render_ws = ws
+        return ws
+
     def _rebuild(self, validate: bool = True):
         """K1 -> K2 -> K3 -> K5 (see module docstring)."""
         L, n, s = self._L, self.n, stream_ptr()
+        self.version = getattr(self, "version", 0) + 1
         self._status.copy_(_lib.new_status(self.device))
         hb = (torch.empty(6, dtype=torch.float64)).numpy()
         check(L.gsx_prepare(ptr(self.params), n, self.sigma_eps, ptr(self.arena),
@@ -125,6 +136,7 @@ class Scene:
         scene bounds stay on the device; validation errors are not raised
         (the optimizer's projection keeps records valid)."""
         L, n, s = self._L, self.n, stream_ptr()
+        self.version = getattr(self, "version", 0) + 1
         check(L.gsx_prepare(ptr(self.params), n, self.sigma_eps, ptr(self.arena),
                             ptr(self._status), None, s), "prepare")
         check(L.gsx_scene_get(ptr(self.arena), n, 4, ptr(self.bounds_t), s), "bounds")

@@ -1,21 +1,25 @@
-"""Scene / camera file ingestion (scene_io.py of the reference).
+"""Scene / camera file ingestion (the file formats of the reference's
+scene_io.py).
 
 * `.gsx` records: `scene.save_scene` / `scene.load_scene` (bit-exact).
-* Cameras JSON: `save_cameras` / `load_cameras` (scene_io.py:114-155), same
-  file layout and errors.
-* 3DGS PLY: `load_ply_scene` (scene_io.py:287-327) parses the vertex table
-  with numpy (ascii or binary little-endian, scene_io.py:330-380), converts
-  all rows at once to the 87-float record layout exactly as the reference's
-  GaussianShape / AppearanceCoeffs ingestion does (quaternion normalized in
-  float64, scales exp'd and clamped at S_MIN, sigma~ = -ln(1 - alpha)/dt_ref
-  with alpha = clip(sigmoid(opacity), 1e-6, 1 - 1e-6), SH DC from f_dc, lobes
-  of `AppearanceCoeffs.constant`), and hands the [N,87] float32 block to the
-  device in one copy (`Scene.from_records`).
-* `export_density_ply` (scene_io.py:383-398).
+* Cameras JSON (schema of scene_io.py:114-155): a table-driven codec
+  (`_CAMERA_SCHEMA`) -- one entry per JSON key with its Camera attribute,
+  converter and default -- used by both `save_cameras` and `load_cameras`.
+* 3DGS PLY (scene_io.py:287-380): `read_ply_vertices` parses the header into
+  an element table, then decodes the vertex block in one shot (a structured
+  numpy dtype for binary little-endian, `np.loadtxt` over the vertex lines for
+  ascii).  `ply_records` converts all rows at once to the 87-float record
+  layout exactly as the reference's GaussianShape / AppearanceCoeffs
+  ingestion does (quaternion normalized in float64, scales exp'd and clamped
+  at S_MIN, sigma~ = -ln(1 - alpha)/dt_ref with alpha = clip(sigmoid(opacity),
+  1e-6, 1 - 1e-6), SH DC from f_dc, lobes of `AppearanceCoeffs.constant`) and
+  hands the [N,87] float32 block to the device in one copy
+  (`Scene.from_records`).
 """
 
 from __future__ import annotations
 
+import io
 import json
 from pathlib import Path
 
@@ -31,86 +35,127 @@ N_SH, N_SG = 9, 7
 
 
 # -- cameras -----------------------------------------------------------------
+def _vec(n):
+    def conv(v):
+        a = np.asarray(v, dtype=float)
+        if a.shape != (n,):
+            raise ValueError(f"expected {n} numbers, got shape {a.shape}")
+        return a
+    return conv
+
+
+# (JSON key, Camera attribute, parse, dump, default or None when required)
+_CAMERA_SCHEMA = (
+    ("center", "center", _vec(3), lambda v: [float(x) for x in v], None),
+    ("quat", "quat", _vec(4), lambda v: [float(x) for x in v], None),
+    ("focal_px", "focal", float, float, None),
+    ("width", "width", int, int, None),
+    ("height", "height", int, int, None),
+    ("t_near", "t_near", float, float, 1e-4),
+    ("t_far", "t_far", float, float, 1e6),
+)
+
+
+def camera_to_json(cam: Camera) -> dict:
+    return {key: dump(getattr(cam, attr)) for key, attr, _, dump, _ in _CAMERA_SCHEMA}
+
+
+def camera_from_json(entry: dict) -> Camera:
+    kw = {}
+    for key, attr, parse, _, default in _CAMERA_SCHEMA:
+        if key in entry:
+            kw[attr] = parse(entry[key])
+        elif default is None:
+            raise KeyError(f"camera entry lacks {key!r}")
+        else:
+            kw[attr] = default
+    return Camera(**kw)
+
+
 def save_cameras(cameras, path):
-    out = {"cameras": [{"center": list(map(float, c.center)), "quat": list(map(float, c.quat)),
-                        "focal_px": c.focal, "width": c.width, "height": c.height,
-                        "t_near": c.t_near, "t_far": c.t_far} for c in cameras]}
-    Path(path).write_text(json.dumps(out, indent=2) + "\n")
+    doc = {"cameras": [camera_to_json(c) for c in cameras]}
+    Path(path).write_text(json.dumps(doc, indent=2) + "\n")
 
 
 def load_cameras(path) -> list:
+    """Cameras of a JSON file; ParseError if unreadable, ValidationError
+    (with the entry index as `record`) for a malformed entry or an empty list."""
     try:
-        data = json.loads(Path(path).read_text())
+        doc = json.loads(Path(path).read_text())
     except (OSError, json.JSONDecodeError) as e:
         raise ParseError(f"cannot read camera file: {e}") from e
-    cams = []
-    for i, c in enumerate(data.get("cameras", [])):
-        try:
-            cams.append(Camera(center=np.asarray(c["center"], dtype=float),
-                               quat=np.asarray(c["quat"], dtype=float),
-                               focal=float(c["focal_px"]), width=int(c["width"]),
-                               height=int(c["height"]), t_near=float(c.get("t_near", 1e-4)),
-                               t_far=float(c.get("t_far", 1e6))))
-        except (KeyError, ValueError) as e:
-            raise ValidationError(str(e), record=i) from e
-    if not cams:
+    entries = doc.get("cameras", []) if isinstance(doc, dict) else []
+    if not entries:
         raise ValidationError("camera file lists no cameras")
-    return cams
+    out = []
+    for idx, entry in enumerate(entries):
+        try:
+            out.append(camera_from_json(entry))
+        except (KeyError, ValueError, TypeError) as e:
+            raise ValidationError(str(e), record=idx) from e
+    return out
 
 
 # -- PLY ---------------------------------------------------------------------
-_PLY_SIZES = {b"float": "<f4", b"float32": "<f4", b"double": "<f8", b"float64": "<f8"}
+_PLY_TYPES = {"float": "<f4", "float32": "<f4", "double": "<f8", "float64": "<f8"}
 PLY_REQUIRED = ["x", "y", "z", "rot_0", "rot_1", "rot_2", "rot_3", "scale_0", "scale_1",
                 "scale_2", "opacity", "f_dc_0", "f_dc_1", "f_dc_2"]
 
 
+def _ply_header(blob: bytes):
+    """(format, [(element name, count, [(property name, type)])], payload offset)."""
+    if not blob.startswith(b"ply"):
+        raise ParseError("not a PLY file")
+    end = blob.find(b"end_header")
+    if end < 0:
+        raise ParseError("unexpected end of PLY header")
+    body = blob.find(b"\n", end)
+    body = len(blob) if body < 0 else body + 1
+    fmt, elements = None, []
+    for raw in blob[:end].decode("ascii", "replace").splitlines()[1:]:
+        tok = raw.split()
+        if not tok or tok[0] in ("comment", "obj_info"):
+            continue
+        if tok[0] == "format" and len(tok) > 1:
+            fmt = tok[1]
+        elif tok[0] == "element" and len(tok) > 2:
+            elements.append((tok[1], int(tok[2]), []))
+        elif tok[0] == "property" and elements:
+            elements[-1][2].append((tok[-1], tok[1]))
+    return fmt, elements, body
+
+
 def read_ply_vertices(path):
     """Vertex table of a PLY file: (names, float64 [n, k]); float/double
-    properties, ascii or binary little-endian (scene_io.py:330-380)."""
-    with open(path, "rb") as f:
-        if f.readline().strip() != b"ply":
-            raise ParseError("not a PLY file")
-        fmt, n_vertex, names, types = None, None, [], []
-        while True:
-            line = f.readline()
-            if not line:
-                raise ParseError("unexpected end of PLY header")
-            parts = line.split()
-            if not parts:
-                continue
-            if parts[0] == b"format":
-                fmt = parts[1]
-            elif parts[0] == b"element":
-                if parts[1] == b"vertex":
-                    n_vertex = int(parts[2])
-                elif n_vertex is not None:
-                    break  # only the vertex element is read
-            elif parts[0] == b"property" and n_vertex is not None:
-                if parts[1] not in _PLY_SIZES:
-                    raise ParseError(f"unsupported property type {parts[1]!r}")
-                types.append(parts[1])
-                names.append(parts[2].decode())
-            elif parts[0] == b"end_header":
-                break
-        if fmt not in (b"ascii", b"binary_little_endian"):
-            raise ParseError(f"unsupported PLY format {fmt!r}")
-        if n_vertex is None or not names:
-            raise ParseError("PLY has no vertex element")
-        if fmt == b"ascii":
-            rows = []
-            for _ in range(n_vertex):
-                vals = f.readline().split()
-                if len(vals) != len(names):
-                    raise ParseError("short PLY vertex row")
-                rows.append([float(v) for v in vals])
-            data = np.array(rows, dtype=np.float64).reshape(n_vertex, len(names))
-        else:
-            dtype = np.dtype([(nm, _PLY_SIZES[t]) for nm, t in zip(names, types)])
-            raw = np.frombuffer(f.read(dtype.itemsize * n_vertex), dtype=dtype)
-            if raw.shape[0] != n_vertex:
-                raise ParseError("truncated PLY payload")
-            data = np.stack([raw[nm].astype(np.float64) for nm in names], axis=1)
-    return names, data
+    properties, ascii or binary little-endian (the subset scene_io.py:330-380
+    accepts).  Only the vertex element is decoded; it must be the first
+    element of the file."""
+    blob = Path(path).read_bytes()
+    fmt, elements, body = _ply_header(blob)
+    if fmt not in ("ascii", "binary_little_endian"):
+        raise ParseError(f"unsupported PLY format {fmt!r}")
+    if not elements or elements[0][0] != "vertex" or not elements[0][2]:
+        raise ParseError("PLY has no vertex element")
+    _, count, props = elements[0]
+    for _, t in props:
+        if t not in _PLY_TYPES:
+            raise ParseError(f"unsupported property type {t!r}")
+    names = [nm for nm, _ in props]
+    if fmt == "binary_little_endian":
+        rec = np.dtype([(nm, _PLY_TYPES[t]) for nm, t in props])
+        if len(blob) - body < rec.itemsize * count:
+            raise ParseError("truncated PLY payload")
+        table = np.frombuffer(blob, dtype=rec, count=count, offset=body)
+        data = np.empty((count, len(names)), dtype=np.float64)
+        for i, nm in enumerate(names):
+            data[:, i] = table[nm]
+        return names, data
+    lines = blob[body:].decode("ascii", "replace").splitlines()
+    rows = [ln for ln in lines if ln.strip()][:count]
+    if len(rows) < count or any(len(ln.split()) != len(names) for ln in rows):
+        raise ParseError("short PLY vertex row")
+    data = np.loadtxt(io.StringIO("\n".join(rows)), dtype=np.float64, ndmin=2)
+    return names, data.reshape(count, len(names))
 
 
 def ply_records(path, sigma_eps: float = DEFAULT_SIGMA_EPS) -> np.ndarray:
@@ -147,14 +192,3 @@ def load_ply_scene(path, sigma_eps: float = DEFAULT_SIGMA_EPS, device=None) -> S
     device: x/y/z, rot_0..3 (scalar first), scale_0..2 (log scales), opacity
     (pre-sigmoid), f_dc_0..2 (SH DC)."""
     return Scene.from_records(ply_records(path, sigma_eps), sigma_eps=sigma_eps, device=device)
-
-
-def export_density_ply(path, means, counts):
-    """ASCII PLY point cloud with a per-point neighbor-count scalar."""
-    means = np.asarray(means, dtype=float).reshape(-1, 3)
-    counts = np.asarray(counts).reshape(-1)
-    lines = ["ply", "format ascii 1.0", f"element vertex {len(means)}", "property float x",
-             "property float y", "property float z", "property float density", "end_header"]
-    for m, c in zip(means, counts):
-        lines.append(f"{m[0]} {m[1]} {m[2]} {float(c)}")
-    Path(path).write_text("\n".join(lines) + "\n")

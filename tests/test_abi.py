@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for f in funcs:
         assert hasattr(L, f), f
     assert sorted(_lib.EXPORTED) == funcs
-    assert L.gsx_abi_version() == 1
+    assert L.gsx_abi_version() == 2
     assert L.gsx_status_string(0) == b"ok"
     assert L.gsx_scene_arena_bytes(1000) > 1000 * 87 * 4
     assert L.gsx_sort_workspace_bytes(1 << 20) > 0
@@ -46,7 +46,7 @@ def test_size_queries_and_argument_errors_without_gpu():
     cam.width = cam.height = 4
     cam.focal = 1.0
     rc = L.gsx_render_forward(None, None, 10, ctypes.byref(cam), ctypes.byref(cfg), 0, 1, None,
-                              None, None, None, None, None)
+                              None, None, None, None, 0, None, None)
     assert rc == _lib.GSX_ERR_ARG  # t_eps must be in (0, 1)
     assert L.gsx_image_loss(None, None, 8, 8, 3, 0.2, None, None, None, None) == _lib.GSX_ERR_ARG
 

@@ -1,0 +1,129 @@
+"""Parity at the benchmark configurations (BASELINE.json configs 2-4), not
+just at test sizes: the frames bench.py times are compared with the float64
+oracle on stratified pixel subsets.
+
+* C3 (1M Gaussians, 1920x1080, adaptive + ESS -- the headline frame) and C4
+  (3M, 1237x822): the plain forward bench.py times (silhouette-screened) on
+  every k-th pixel per axis against `oracle.OracleScene.march_rays` on the
+  same rays (renderer.py:263-358 semantics).  Tolerances (north star): max
+  |RGB| 1e-4, max |T| 1e-4, depth |dD| <= 1e-4 max(1, D).
+* The screen only skips (lane, primitive) pairs whose contribution is exactly
+  zero, in the same summation order, so the screened frame must equal the
+  unscreened one bit for bit (a wrongly screened-out pair would show).
+* C2 (300k, 800x800, uniform + ESS, white background) backward: dL/dI is
+  non-zero only on a sparse pixel mask, so the oracle's analytic float64
+  backward (oracle/gsray_oracle.c, FD-pinned in test_oracle_grad.py) is
+  affordable at full scene size.  Element-wise: every gradient entry with
+  |g| >= 1e-3 max|g| of its parameter group agrees to relative 1e-3, and
+  every entry to relative 1e-3 above an absolute floor of 1e-6 max|g| of its
+  group (the fp32 accumulation floor).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+THREADS = len(os.sched_getaffinity(0))
+
+
+def _setup(name):
+    import bench
+    import paper_2509_07782_b200 as G
+
+    rec, eps, cam_kw, cfg_kw, _ = bench.workload(name)
+    scene = G.Scene.from_records(rec, sigma_eps=eps)
+    G.reorder_by_morton(scene)
+    cam = bench.make_camera(G, cam_kw)
+    cfg = G.RenderConfig(**cfg_kw)
+    return G, rec, eps, scene, cam, cfg, cfg_kw
+
+
+def _pixels(cam, stride, oy, ox):
+    rays = O.camera_rays(cam.center, cam.quat, cam.focal, cam.width, cam.height)
+    rays = rays.reshape(cam.height, cam.width, 8)[oy::stride, ox::stride]
+    py, px = np.mgrid[oy:cam.height:stride, ox:cam.width:stride]
+    return rays.reshape(-1, 8), py.ravel(), px.ravel()
+
+
+def _forward_subset(name, stride, oy, ox):
+    G, rec, eps, scene, cam, cfg, cfg_kw = _setup(name)
+    rgb, depth, trans, _ = G.render(scene, cam, cfg)
+    rgb0, depth0, trans0, _ = G.render(scene, cam, cfg, screen=False)
+    rgb, depth, trans = rgb.cpu().numpy(), depth.cpu().numpy(), trans.cpu().numpy()
+    # screened == unscreened, bit for bit
+    np.testing.assert_array_equal(rgb, rgb0.cpu().numpy())
+    np.testing.assert_array_equal(trans, trans0.cpu().numpy())
+    np.testing.assert_array_equal(depth, depth0.cpu().numpy())
+    rays, py, px = _pixels(cam, stride, oy, ox)
+    osc = O.OracleScene(rec, eps)
+    R, T, D, _ = osc.march_rays(rays, O.OCfg.make(**cfg_kw), clip=True, threads=THREADS)
+    err_rgb = np.abs(rgb[py, px] - R).max()
+    err_t = np.abs(trans[py, px] - T).max()
+    err_d = (np.abs(depth[py, px] - D) / np.maximum(1.0, D)).max()
+    assert err_rgb < 1e-4, err_rgb
+    assert err_t < 1e-4, err_t
+    assert err_d < 1e-4, err_d
+    # the subset must exercise the frame: hits, misses and partial opacity
+    assert (T < 0.5).sum() > 0.1 * len(T) and (T > 0.999).sum() > 0
+    return len(rays)
+
+
+def test_c3_headline_frame_vs_oracle():
+    # every 24th pixel per axis of the 1080p frame: 45 x 80 = 3600 rays
+    assert _forward_subset("c3", 24, 11, 7) == 3600
+
+
+def test_c4_frame_vs_oracle():
+    # every 32nd pixel per axis of 1237 x 822: 26 x 39 = 1014 rays
+    assert _forward_subset("c4", 32, 5, 13) == 26 * 39
+
+
+def test_c2_backward_sparse_mask_vs_oracle():
+    import torch
+
+    G, rec, eps, scene, cam, cfg, cfg_kw = _setup("c2")
+    H, W = cam.height, cam.width
+    rays, py, px = _pixels(cam, 40, 17, 23)  # 20 x 20 = 400 pixels
+    rng = np.random.default_rng(3)
+    gC = np.zeros((H, W, 3))
+    gT = np.zeros((H, W))
+    gD = np.zeros((H, W))
+    gC[py, px] = rng.normal(size=(len(py), 3))
+    gT[py, px] = rng.normal(size=len(py))
+    gD[py, px] = 0.1 * rng.normal(size=len(py))
+    t = lambda a: torch.as_tensor(a, dtype=torch.float32, device="cuda")  # noqa: E731
+    osc = O.OracleScene(rec, eps)
+    _, _, _, g_ref = osc.backward_rays(rays, O.OCfg.make(**cfg_kw), gC[py, px], gD[py, px],
+                                       gT[py, px], clip=True)
+    uids = scene.uids  # GPU storage position -> original record index
+    for log in (None, "full"):
+        lg = None
+        if log:
+            lg = G.MarchLog(cam)
+            for _ in range(2):
+                G.render(scene, cam, cfg, log=lg)
+                if not lg.ensure():
+                    break
+        rgb, depth, trans, _ = G.render(scene, cam, cfg, log=lg)
+        if lg is not None:
+            assert not lg.usage()[1]
+        g = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg)
+        g_gpu = np.empty_like(g_ref)
+        g_gpu[uids] = g.cpu().numpy()
+        for name, (a, b) in {"mean": (0, 3), "quat": (3, 7), "scale": (7, 10),
+                             "sigma": (10, 11), "sh": (11, 38), "axis": (38, 59),
+                             "sharp": (59, 66), "amp": (66, 87)}.items():
+            A, B = g_gpu[:, a:b], g_ref[:, a:b]
+            gmax = np.abs(B).max()
+            assert gmax > 0, name
+            big = np.abs(B) >= 1e-3 * gmax
+            rel = np.abs(A - B)[big] / np.abs(B)[big]
+            assert rel.max() <= 1e-3, (log, name, rel.max(), int(big.sum()))
+            # every entry: relative 1e-3 above an absolute floor of 1e-6 max|g|
+            err = np.abs(A - B) - 1e-3 * np.abs(B)
+            assert err.max() <= 1e-6 * gmax, (log, name, err.max(), gmax)

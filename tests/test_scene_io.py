@@ -100,15 +100,21 @@ def test_ply_errors(tmp_path):
     assert e.value.record == 1
 
 
-def test_export_density(tmp_path):
-    p = tmp_path / "density.ply"
-    S.export_density_ply(p, np.zeros((3, 3)), [1, 2, 3])
-    text = p.read_text().splitlines()
-    assert text[0] == "ply"
-    assert "property float density" in text
-    assert len(text) == 8 + 3
+def test_ply_reader_header_forms(tmp_path):
+    # comments, a trailing face element and a truncated binary payload
+    p = tmp_path / "v.ply"
+    p.write_text("ply\nformat ascii 1.0\ncomment made by hand\nelement vertex 3\n"
+                 "property float x\nproperty float y\nproperty float z\n"
+                 "property float density\nelement face 0\n"
+                 "property list uchar int vertex_indices\nend_header\n"
+                 "0 0 0 1\n0 0 0 2\n0 0 0 3\n")
     names, data = S.read_ply_vertices(p)
     assert names == ["x", "y", "z", "density"] and data[:, 3].tolist() == [1.0, 2.0, 3.0]
+    b = tmp_path / "t.ply"
+    b.write_bytes(b"ply\nformat binary_little_endian 1.0\nelement vertex 2\n"
+                  b"property float x\nend_header\n" + np.zeros(1, "<f4").tobytes())
+    with pytest.raises(ParseError):
+        S.read_ply_vertices(b)
 
 
 def test_cameras_reference_file_and_roundtrip(tmp_path):
