@@ -267,21 +267,94 @@ def cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s: float = 15.0, steps: int = 
     per_ray = dt / len(probe)
     want = target_s / max(steps, 1) / per_ray
     stride = int(max(1, min(256, math.floor(math.sqrt(total / max(want, 1.0))))))
-    times, nrays = [], 0
+    times, nrays, last = [], 0, None
     for k in range(steps):
         rays = cpu_rays(cam_kw, stride, offset0 + k)
         t0 = time.time()
-        osc.march_rays(rays, cfg, clip=True, threads=threads)
+        out = osc.march_rays(rays, cfg, clip=True, threads=threads)
         times.append(time.time() - t0)
         nrays += len(rays)
+        last = (offset0 + k, stride, out)
     value = nrays / sum(times) / 1e6
     return {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "port",
             "sample": f"every {stride}th pixel per axis of the frame ({nrays // max(steps, 1)} rays/step, "
                       f"{steps} step(s), {sum(times):.1f} s); oracle scene prep+BVH {build_s:.1f} s",
-            "seconds": sum(times)}
+            "seconds": sum(times), "last": last}
+
+
+def sample_pixels(cam_kw, stride: int, offset: int):
+    """(py, px) of the pixels cpu_rays(cam_kw, stride, offset) returns, in order."""
+    oy, ox = divmod(offset, stride)
+    py, px = np.mgrid[oy % stride:cam_kw["height"]:stride, ox:cam_kw["width"]:stride]
+    return py.ravel(), px.ravel()
+
+
+def parity_block(cb, cam_kw, rgb, depth, trans):
+    """The oracle's outputs on the cpu_baseline sample vs the same pixels of
+    the GPU frame the timed region rendered (tolerances: north star)."""
+    offset, stride, (R, T, D, _) = cb["last"]
+    py, px = sample_pixels(cam_kw, stride, offset)
+    g_rgb = rgb.cpu().numpy()[py, px]
+    g_t = trans.cpu().numpy()[py, px]
+    g_d = depth.cpu().numpy()[py, px]
+    out = {"n_rays": int(len(py)), "max_abs_rgb": float(np.abs(g_rgb - R).max()),
+           "max_abs_T": float(np.abs(g_t - T).max()),
+           "max_rel_depth": float((np.abs(g_d - D) / np.maximum(1.0, D)).max()),
+           "sample": f"every {stride}th pixel per axis (offset {offset})",
+           "tolerance": {"rgb": 1e-4, "T": 1e-4, "depth_rel": 1e-4}}
+    out["pass"] = bool(out["max_abs_rgb"] < 1e-4 and out["max_abs_T"] < 1e-4
+                       and out["max_rel_depth"] < 1e-4)
+    return out
 
 
 # ----------------------------------------------------------------------------- main
+def self_launch(n: int):
+    """`--gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
+def calibrate(L, _lib, dev, s):
+    """FP32 (dependent FFMA chains) and SFU (MUFU.EX2 chains) issue rates of
+    this device at its current clocks, from the library's calibration kernels."""
+    import ctypes
+
+    import torch
+
+    sink = torch.empty(148 * 8 * 256 * 2, dtype=torch.float32, device=dev)
+    out = {}
+    for key, fn, iters in (("fp32_tflops", L.gsx_calibrate_fp32, 20000),
+                           ("sfu_tops", L.gsx_calibrate_sfu, 8000)):
+        fl = ctypes.c_double(0)
+        fn(iters // 10, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fn(iters, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
+        e1.record(s)
+        torch.cuda.synchronize()
+        out[key] = fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    return out
+
+
+def ncu_evidence(config: str):
+    """Per-launch DRAM bytes and pipe utilisations of the timed kernel from the
+    committed ncu capture (profiles/traffic.json; never measured in this run)."""
+    try:
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return tr.get(config, {})
+    except Exception:
+        return {}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -296,9 +369,13 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
     rec, eps, cam_kw, cfg_kw, desc = workload(args.config)
     H, W = cam_kw["height"], cam_kw["width"]
@@ -323,6 +400,8 @@ def main():
                     "d2h_bytes_per_step": 0}}), flush=True)
         return
 
+    import ctypes
+
     import torch
 
     torch.cuda.set_device(local_rank)
@@ -332,10 +411,12 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_2509_07782_b200 as G
     from paper_2509_07782_b200 import _lib
+    from paper_2509_07782_b200.train import gather_tiles
 
     dev = torch.device("cuda", local_rank)
     cam = make_camera(G, cam_kw)
     cfg = G.RenderConfig(**cfg_kw)
+    L = _lib.lib()
 
     # ---- scene upload + build (K1-K5) + Morton reorder
     params_host = torch.from_numpy(rec.astype(np.float32)).pin_memory()
@@ -357,50 +438,32 @@ def main():
     build_ms = e0.elapsed_time(e1) / 5
 
     # ---- algorithmic work counters (untimed stats pass)
-    rgb, depth, trans, st = G.render(scene, cam, cfg, stats=True)
+    st = G.render(scene, cam, cfg, stats=True)[3]
     torch.cuda.synchronize()
     cnt = st.cpu().numpy().astype(np.float64)
     keys = ["rays", "samples", "segments", "segments_skipped", "closest_hit_calls", "node_visits",
             "aabb_hits", "ellipsoid_hits", "pairs", "composited"]
     counters = dict(zip(keys, cnt.tolist()))
-    # FLOPs/ray = 33 P + 15 S + 165 Cr + 12 V
+    # FLOPs/ray = 33 P + 15 S + 165 Cr + 12 V; SFU/ray = P + 2 S + 7 Cr
     flops_frame = (33 * counters["pairs"] + 15 * counters["samples"] +
                    165 * counters["ellipsoid_hits"] + 12 * counters["node_visits"])
+    sfu_frame = counters["pairs"] + 2 * counters["samples"] + 7 * counters["ellipsoid_hits"]
+    cal = calibrate(L, _lib, dev, s)
 
-    # ---- FP32 roofline denominator: measured FFMA issue rate
-    sink = torch.empty(148 * 8 * 256 * 2, dtype=torch.float32, device=dev)
-    import ctypes
-
-    fl = ctypes.c_double(0)
-    L = _lib.lib()
-    L.gsx_calibrate_fp32(2000, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
-    torch.cuda.synchronize()
-    e0.record(s)
-    L.gsx_calibrate_fp32(20000, _lib.ptr(sink), ctypes.byref(fl), _lib.stream_ptr())
-    e1.record(s)
-    torch.cuda.synchronize()
-    fp32_peak = fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12
-
-    # ---- timed forward
+    # ---- timed forward (the screened plain forward, K6)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     rgb = torch.zeros((H, W, 3), device=dev)
     depth = torch.zeros((H, W), device=dev)
     trans = torch.zeros((H, W), device=dev)
     tb, ts = (rank, world) if world > 1 else (0, 1)
-    from paper_2509_07782_b200.train import assemble_tiles
 
-    def step(out=None):
-        # N > 1: every rank renders its interleaved tiles; the frame is then
-        # assembled on every rank (one NCCL all-reduce of disjoint tiles)
-        out = rgb if out is None else out
+    def step(out=(rgb, depth, trans)):
+        # N > 1: every rank renders its interleaved tiles, then the frame is
+        # assembled on every rank (all-gather of the ranks' own tiles)
+        G.render(scene, cam, cfg, tile_begin=tb, tile_stride=ts, rgb=out[0], depth=out[1],
+                 trans=out[2])
         if world > 1:
-            out.zero_()
-            depth.zero_()
-            trans.zero_()
-        G.render(scene, cam, cfg, tile_begin=tb, tile_stride=ts, rgb=out, depth=depth,
-                 trans=trans)
-        if world > 1:
-            assemble_tiles([out, depth, trans])
+            gather_tiles(list(out), cam.width, cam.height)
 
     with ClockSampler(local_rank) as clk:
         for _ in range(args.warmup):
@@ -426,16 +489,20 @@ def main():
         tot_ms = float(t.item())
     ms = tot_ms / args.steps
     mrays = H * W / (ms * 1e-3) / 1e6
+    frame = (rgb.clone(), depth.clone(), trans.clone())
 
-    # ---- e2e through the public API: camera from host, frame back to pinned host
-    # Frames are double-buffered: frame k's device->host read runs on a copy
-    # stream while frame k+1 renders; frame k+2 reuses the buffer only after
-    # that read has finished.  Every frame is read back inside the timed region.
-    host_rgb = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
-    dev_rgb = [rgb, torch.zeros_like(rgb)]
+    # ---- e2e through the C ABI: the host camera + config structs go in with
+    # every call (gsx_render_forward copies them into the launch), the whole
+    # frame (rgb, depth, T) comes back into pinned host memory.  Frames are
+    # double-buffered: frame k's device->host read runs on a copy stream while
+    # frame k+1 renders; every frame is read back inside the timed region.
+    host = [[torch.empty(t.shape, dtype=torch.float32).pin_memory() for t in frame]
+            for _ in range(2)]
+    devb = [[rgb, depth, trans], [torch.zeros_like(t) for t in frame]]
     cs = torch.cuda.Stream(device=dev)
     rendered = [torch.cuda.Event() for _ in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
+    ws = scene.render_workspace()
 
     def e2e_frames(n):
         for k in range(n):
@@ -443,11 +510,18 @@ def main():
             if k >= 2:
                 s.wait_event(copied[b])
             flush.zero_()
-            step(dev_rgb[b])
+            cam_c, cfg_c = cam.to_c(), cfg.to_c()  # host structs, by pointer
+            _lib.check(L.gsx_render_forward(
+                _lib.ptr(scene.arena), _lib.ptr(scene.bvh_arena), scene.n, ctypes.byref(cam_c),
+                ctypes.byref(cfg_c), tb, ts, *(_lib.ptr(t) for t in devb[b]), None,
+                _lib.ptr(ws), ws.numel(), None, _lib.stream_ptr(s)), "render_forward")
+            if world > 1:
+                gather_tiles(devb[b], cam.width, cam.height)
             rendered[b].record(s)
             cs.wait_event(rendered[b])
             with torch.cuda.stream(cs):
-                host_rgb[b].copy_(dev_rgb[b], non_blocking=True)
+                for h, d in zip(host[b], devb[b]):
+                    h.copy_(d, non_blocking=True)
                 copied[b].record(cs)
         s.wait_stream(cs)
 
@@ -460,16 +534,30 @@ def main():
     e1.record(s)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps  # includes the L2 flush (conservative)
-    assert torch.equal(host_rgb[(args.steps - 1) % 2], dev_rgb[(args.steps - 1) % 2].cpu())
+    last = (args.steps - 1) % 2
+    assert all(torch.equal(h, d.cpu()) for h, d in zip(host[last], devb[last]))
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e6, "unit": "Mrays/s",
-           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": H * W * 3 * 4,
-           "note": ("camera passed by value in the launch parameters; every frame read "
-                    "back to pinned host memory (double-buffered: frame k's read overlaps "
-                    "frame k+1's render); includes a 256 MiB L2 flush per frame")}
+           "h2d_bytes_per_step": ctypes.sizeof(_lib.CameraC) + ctypes.sizeof(_lib.RenderCfg),
+           "d2h_bytes_per_step": sum(t.numel() * 4 for t in frame),
+           "api": "gsx_render_forward (C ABI, include/gsx.h) with host gsx_camera / "
+                  "gsx_render_cfg structs; rgb + depth + T read back to pinned host memory",
+           "note": ("h2d = the camera + config structs the call copies into the launch (the "
+                    "frame's only per-step inputs: the scene is resident); double-buffered "
+                    "read-back; includes a 256 MiB L2 flush per frame")}
+
+    # ---- the reference-facing drop-in: render_image -> float64 numpy + lazy stats
+    ri = []
+    if world == 1:
+        for _ in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            img, _st = G.render_image(scene, cam, cfg)
+            ri.append(1e3 * (time.perf_counter() - t0))
+        assert np.array_equal(img, frame[0].double().cpu().numpy())
 
     train = None
     if not args.no_train:
@@ -481,39 +569,66 @@ def main():
         dist.destroy_process_group()
         return
     achieved = flops_frame / (ms * 1e-3) / 1e12
-    traffic = None
-    try:  # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu capture
-        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text())
-        traffic = tr.get(args.config, {}).get("k_render_camera")
-    except Exception:
-        pass
-    roof = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp32_peak, "traffic": traffic,
+    ev = ncu_evidence(args.config)
+    hbm_alg = 348.0 * rec.shape[0] + 128.0 * rec.shape[0] / 3 + 20.0 * H * W
+    pk = peaks()
+    roof = {"bound": "fp32", "achieved": achieved, "peak": cal["fp32_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / cal["fp32_tflops"], "traffic": ev.get("dram_bytes"),
             "traffic_unit": "bytes per launch (ncu --set full, profiles/traffic.json)",
             "peak_source": "measured FFMA loop (gsx_calibrate_fp32) in this run",
             "flops_per_frame": flops_frame,
-            "flops_model": ("33*pairs + 15*samples + 165*ellipsoid_hits + 12*node_visits "
-                            "(SURVEY 8(d)); pairs = samples x AABB overlaps per Alg. 1 "
-                            "segment; samples / ellipsoid_hits in the reference's RenderStats "
-                            "semantics (incl. its buffer-overflow sub-collects)")}
+            "flops_model": ("reference-equivalent work: 33*pairs + 15*samples + "
+                            "165*ellipsoid_hits + 12*node_visits (SURVEY 8(d)); pairs = samples "
+                            "x AABB overlaps per Alg. 1 segment incl. the reference's inverted "
+                            "'phantom' overlaps; samples / ellipsoid_hits in RenderStats "
+                            "semantics.  It credits work the kernel skips exactly (phantom and "
+                            "screened pairs), so it is a reference-equivalent rate, not pipe use "
+                            "-- see `pipes`"),
+            "sfu": {"achieved": sfu_frame / (ms * 1e-3) / 1e12, "peak": cal["sfu_tops"],
+                    "unit": "Tops/s", "frac": sfu_frame / (ms * 1e-3) / 1e12 / cal["sfu_tops"],
+                    "model": "pairs + 2*samples + 7*ellipsoid_hits exponentials per frame",
+                    "peak_source": "measured MUFU.EX2 loop (gsx_calibrate_sfu) in this run"},
+            "hbm": {"achieved_formula_gbs": hbm_alg / (ms * 1e-3) / 1e9,
+                    "achieved_ncu_gbs": (ev["dram_bytes"] / (ev["ms"] * 1e-3) / 1e9
+                                         if ev.get("dram_bytes") and ev.get("ms") else None),
+                    "peak_gbs": pk.get("hbm_gbs"),
+                    "formula": "348*N + 128*N/3 (4-wide BVH) + 20*H*W bytes per frame "
+                               "(every primitive and node touched once: an upper bound)"},
+            "pipes": ev.get("pipes")}
     out = {
         "metric": METRIC, "value": mrays, "unit": "Mrays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "fps": 1e3 / ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config, "roofline": roof, "e2e": e2e,
-        "gpu_launches": args.steps, "clocks": clk.summary(),
-        "build_ms": build_ms, "setup_s": setup_s,
+        "gpu_launches": 2 * args.steps, "gpu_launches_note": "k_view_conics + k_render_screened "
+        "per frame", "clocks": clk.summary(), "build_ms": build_ms, "setup_s": setup_s,
         "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
         "step_ms": step_ms,
     }
+    if ri:
+        out["render_image_ms"] = {"median": float(np.median(ri)), "runs": ri,
+                                  "note": "G.render_image (drop-in): render + float64 numpy "
+                                          "image on the host, lazy RenderStats (not read)"}
     if train is not None:
         out["train_step"] = train
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline"]["cpu_model"] = cpu_model()
+        out["parity"] = parity_block(cb, cam_kw, *frame)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 if __name__ == "__main__":

@@ -92,6 +92,10 @@ typedef struct {
    Writes sink (one float per thread, grid*block) and returns flops through
    *flops.  Used by bench.py to measure the FP32 roofline denominator. */
 int gsx_calibrate_fp32(int64_t iters, float* sink, double* flops, void* stream);
+/* SFU issue-rate calibration: 8 independent MUFU.EX2 chains per thread over
+   the whole device; *ops = exponentials executed.  The SFU roofline
+   denominator of bench.py. */
+int gsx_calibrate_sfu(int64_t iters, float* sink, double* ops, void* stream);
 
 /* Device status word written by kernels: {status, record/count, capacity, pad}. */
 typedef struct {
@@ -200,6 +204,12 @@ int gsx_closest_hit(const void* scene_arena, const void* bvh_arena, int64_t n,
  * dev_status (nullable): GSX_ERR_STACK if a traversal stack overflowed (the
  * frame is then incomplete). */
 size_t gsx_render_workspace_bytes(int64_t n);
+/* Row-major tile id at tile-sequence position s of a camera launch with
+ * tile_stride `stride` over a tiles_x x tiles_y grid of 16x16 tiles (the
+ * order gsx_render_forward / _logged / backward use; -1 if out of range).
+ * Host-only: hosts that shard or gather frames query it instead of copying
+ * the order. */
+int64_t gsx_tile_id(int64_t s, int64_t tiles_x, int64_t tiles_y, int64_t stride);
 int gsx_render_forward(const void* scene_arena, const void* bvh_arena, int64_t n,
                        const gsx_camera* cam, const gsx_render_cfg* cfg, int64_t tile_begin,
                        int64_t tile_stride, float* rgb, float* depth, float* trans,

@@ -98,6 +98,7 @@ _SIGS = {
     "gsx_collect_segments": (INT, [P, P, I64, P, I64, I64, P, P, P, P]),
     "gsx_closest_hit": (INT, [P, P, I64, P, I64, P, P]),
     "gsx_render_workspace_bytes": (SZ, [I64]),
+    "gsx_tile_id": (I64, [I64, I64, I64, I64]),
     "gsx_render_forward": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, P, I64, P, P]),
     "gsx_render_rays": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
     "gsx_render_rays_stats": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
@@ -111,6 +112,7 @@ _SIGS = {
     "gsx_neighbor_density": (INT, [P, P, I64, D, P, P, P]),
     "gsx_densify_criteria": (INT, [P, P, P, I64, D, P, P, P]),
     "gsx_calibrate_fp32": (INT, [I64, P, P, P]),
+    "gsx_calibrate_sfu": (INT, [I64, P, P, P]),
     "gsx_image_loss_workspace_bytes": (SZ, [I64, I64, I64]),
     "gsx_image_loss": (INT, [P, P, I64, I64, I64, D, P, P, P, P]),
     "gsx_iso_loss": (INT, [P, I64, D, D, P, P, P]),

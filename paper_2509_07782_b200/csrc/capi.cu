@@ -34,3 +34,10 @@ extern "C" const char* gsx_status_string(int status) {
     default: return "unknown status";
   }
 }
+
+// Tile order of camera launches (gsx_tile_at, gsx_common.cuh) for hosts that
+// shard or assemble frames: the host never keeps its own copy of the order.
+extern "C" int64_t gsx_tile_id(int64_t s, int64_t tiles_x, int64_t tiles_y, int64_t stride) {
+  if (tiles_x < 1 || tiles_y < 1 || s < 0 || s >= tiles_x * tiles_y || stride < 1) return -1;
+  return gsx_tile_at(s, tiles_x, tiles_y, stride);
+}

@@ -565,6 +565,22 @@ __global__ void k_ffma(int64_t iters, float* sink) {
   sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = a + d + e + f + g + h;
 }
 
+// SFU calibration: 8 independent MUFU.EX2 chains per thread (the forward's
+// exponentials are ex2.approx)
+__global__ void k_mufu(int64_t iters, float* sink) {
+  float v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = -1e-3f * (float)(threadIdx.x + k);
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ex2_approx(-v[k]) - 1.5f;
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc += v[k];
+  sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 }  // namespace
 
 int gsx_validate_cfg(const gsx_render_cfg* cfg) {
@@ -588,6 +604,16 @@ extern "C" int gsx_calibrate_fp32(int64_t iters, float* sink, double* flops, voi
   return gsx_check_launch();
 }
 
+extern "C" int gsx_calibrate_sfu(int64_t iters, float* sink, double* ops, void* stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int blocks = sms * 8, threads = 256;
+  k_mufu<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, sink);
+  if (ops) *ops = 8.0 * (double)iters * blocks * threads;
+  return gsx_check_launch();
+}
+
 #ifdef GSX_PHASE_PROF
 extern "C" int gsx_phase_times(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, gsx::g_phase, sizeof(unsigned long long) * 16);
@@ -599,6 +625,7 @@ extern "C" int gsx_phase_times(unsigned long long* out, int reset) {
 }
 #endif
 
+// per-render workspace: the per-camera silhouette table, float4[2n]
 extern "C" size_t gsx_render_workspace_bytes(int64_t n) {
   return n > 0 ? (size_t)n * 2 * sizeof(float4) : 0;
 }

@@ -352,7 +352,7 @@ def test_rank_shards_cover_frame(G):
             G.render(c1, cam, cfg, tile_begin=r, tile_stride=world, rgb=rgb)
             got = rgb.cpu().numpy()
             mask = np.zeros((75, 100), dtype=bool)
-            for t in tiles_of_rank(35, r, world, 7):
+            for t in tiles_of_rank(7, 5, r, world):
                 ty, tx = divmod(t, 7)
                 mask[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16] = True
             assert np.all(got[~mask] == -1.0), (world, r)
