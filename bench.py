@@ -482,6 +482,7 @@ def main():
         torch.cuda.synchronize()
         clk.mark_end()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    scene.check_render_status()  # no traversal-stack overflow in any timed frame
     tot_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)

@@ -220,6 +220,26 @@ int gsx_render_rays(const void* scene_arena, const void* bvh_arena, int64_t n,
                     float* rgb, float* depth, float* trans, gsx_stats* stats,
                     gsx_dev_status* dev_status, void* stream);
 
+/* ---- dense oracles (renderer.py:440-493, appearance.py:107-134), float64 ----
+ * gsx_reference_rays: reference_integrate per ray (clip = 0: the ray's own
+ * [t_near, t_far]) or reference_render's clip_ray_to_scene + integrate per
+ * pixel ray (clip = 1; a miss gives the background): midpoint quadrature at
+ * fine_dt against every primitive -- no BVH, no skipping, no termination --
+ * composited as renderer.py:472-480.  rays [m,8] f64 (o, d, t_near, t_far),
+ * background[3], rgb [m,3] f64.  params = the [N,87] f32 records the arena
+ * was prepared from.
+ * gsx_eval_fields: mixture density sigma [m] and density-weighted radiance
+ * color [m,3] (f64) at points [m,3] for directions dirs [m,3], over every
+ * primitive or the storage indices active [n_active] (an out-of-range index:
+ * GSX_ERR_ARG in dev_status).  Zero density gives black. */
+int gsx_reference_rays(const void* scene_arena, const float* params, int64_t n,
+                       const double* rays, int64_t m, int clip, double fine_dt,
+                       const double* background, double* rgb, void* stream);
+int gsx_eval_fields(const void* scene_arena, const float* params, int64_t n,
+                    const double* points, const double* dirs, int64_t m,
+                    const int64_t* active, int64_t n_active, double* sigma, double* color,
+                    gsx_dev_status* dev_status, void* stream);
+
 /* Per-ray RenderStats: per_ray [m,10] u64 = (ray?, samples, segments,
  * segments_skipped, closest_hit_calls, node_visits, aabb_hits, ellipsoid_hits,
  * pairs, composited) of each ray (bench.false_positive_fraction

@@ -1065,6 +1065,179 @@ int oracle_march_rays(void *h, const ocfg *cfg, int64_t m, const double *rays, i
   return OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* dense oracles (renderer.py:440-493, appearance.py:107-134)                */
+/* ------------------------------------------------------------------------ */
+
+/* primitive storage positions in ascending uid (the reference's
+   np.argsort(uids, kind="stable") at renderer.py:456 / appearance.py:122) */
+static int64_t *uid_order(const oscene *s) {
+  int64_t *ord = malloc(sizeof(int64_t) * (s->n > 0 ? s->n : 1));
+  for (int64_t i = 0; i < s->n; ++i) ord[s->uids[i]] = i;  /* uids are a permutation */
+  return ord;
+}
+
+/* renderer.py:440-480 reference_integrate: midpoint quadrature at fine_dt
+   over [t_near, t_far] against the full primitive list (uid order), then the
+   vectorised compositing of lines 472-480 (cumsum, -expm1(-od) exp(-cum),
+   sum over sigma > 0 of (w / sigma) * weighted, exit transmittance x bg). */
+static void reference_integrate(const oscene *s, const int64_t *ord, const double *o,
+                                const double *d, double t_near, double t_far, double fine_dt,
+                                const double *bg, double *out) {
+  for (int k = 0; k < 3; ++k) out[k] = bg[k];
+  if (t_near >= t_far) return;
+  int64_t n = (int64_t)ceil((t_far - t_near) / fine_dt);
+  int64_t m = 0;
+  while (m < n && t_near + ((double)m + 0.5) * fine_dt < t_far) ++m;
+  if (m == 0) return;
+  double *ts = malloc(sizeof(double) * m), *sigma = calloc(m, sizeof(double));
+  double *wsum = calloc(3 * m, sizeof(double));
+  for (int64_t j = 0; j < m; ++j) ts[j] = t_near + ((double)j + 0.5) * fine_dt;
+  for (int64_t a = 0; a < s->n; ++a) {
+    const int64_t i = ord[a];
+    const double *M = s->iso_inv + 9 * i, *mu = s->means + 3 * i;
+    double c[3];
+    int have_c = 0;
+    for (int64_t j = 0; j < m; ++j) {
+      double v[3], y[3];
+      for (int k = 0; k < 3; ++k) v[k] = (o[k] + ts[j] * d[k]) - mu[k];
+      for (int b = 0; b < 3; ++b) y[b] = v[0] * M[3 * b] + v[1] * M[3 * b + 1] + v[2] * M[3 * b + 2];
+      const double q = y[0] * y[0] + y[1] * y[1] + y[2] * y[2];
+      if (!(q <= 1.0)) continue;
+      const double dens = s->sigmas[i] * exp(-0.5 * s->log_ratio[i] * q);
+      if (!have_c) {
+        eval_radiance(s->coeffs + NCOEF * i, d, c, NULL, NULL);
+        have_c = 1;
+      }
+      sigma[j] += dens;
+      for (int k = 0; k < 3; ++k) wsum[3 * j + k] += dens * c[k];
+    }
+  }
+  double cum = 0.0, col[3] = {0, 0, 0}, od = 0.0;
+  for (int64_t j = 0; j < m; ++j) {
+    od = sigma[j] * fine_dt;
+    if (sigma[j] > 0.0) {
+      const double w = -expm1(-od) * exp(-cum);
+      for (int k = 0; k < 3; ++k) col[k] += (w / sigma[j]) * wsum[3 * j + k];
+    }
+    if (j + 1 < m) cum += od;
+  }
+  const double t_exit = exp(-(cum + od));
+  for (int k = 0; k < 3; ++k) out[k] = col[k] + t_exit * bg[k];
+  free(ts);
+  free(sigma);
+  free(wsum);
+}
+
+typedef struct {
+  const oscene *s;
+  const int64_t *ord;
+  const double *rays, *bg;
+  int64_t m, clip;
+  double fine_dt;
+  double *rgb;
+  int64_t next;
+  pthread_mutex_t mu;
+} dense_job;
+
+static void *dense_worker(void *arg) {
+  dense_job *jb = (dense_job *)arg;
+  for (;;) {
+    pthread_mutex_lock(&jb->mu);
+    const int64_t r = jb->next++;
+    pthread_mutex_unlock(&jb->mu);
+    if (r >= jb->m) break;
+    const double *ray = jb->rays + 8 * r;
+    double d[3] = {ray[3], ray[4], ray[5]}, tn = ray[6], tf = ray[7];
+    double *out = jb->rgb + 3 * r;
+    if (jb->clip) {  /* reference_render: clip_ray_to_scene, background on a miss */
+      if (!clip_ray(jb->s, ray, d, ray[6], ray[7], &tn, &tf)) {
+        for (int k = 0; k < 3; ++k) out[k] = jb->bg[k];
+        continue;
+      }
+    } else {  /* Ray.__post_init__ renormalization (renderer.py:60-64) */
+      const double nn = vnorm(d, 3);
+      if (fabs(nn - 1.0) > 1e-9)
+        for (int k = 0; k < 3; ++k) d[k] = d[k] / nn;
+    }
+    reference_integrate(jb->s, jb->ord, ray, d, tn, tf, jb->fine_dt, jb->bg, out);
+  }
+  return NULL;
+}
+
+/* reference_integrate per ray (clip = 0) or reference_render's per-pixel
+   clip + integrate (clip = 1, renderer.py:483-493) over m rays (o, d, t_near,
+   t_far), on `threads` host threads. */
+int oracle_reference_rays(void *h, int64_t m, const double *rays, int64_t clip, double fine_dt,
+                          const double *bg, int64_t threads, double *rgb) {
+  if (!(fine_dt > 0.0)) return ERR_ARG;
+  dense_job jb;
+  memset(&jb, 0, sizeof jb);
+  jb.s = (const oscene *)h;
+  jb.ord = uid_order(jb.s);
+  jb.rays = rays;
+  jb.bg = bg;
+  jb.m = m;
+  jb.clip = clip;
+  jb.fine_dt = fine_dt;
+  jb.rgb = rgb;
+  pthread_mutex_init(&jb.mu, NULL);
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  for (int64_t t = 1; t < threads; ++t) pthread_create(&th[t], NULL, dense_worker, &jb);
+  dense_worker(&jb);
+  for (int64_t t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  pthread_mutex_destroy(&jb.mu);
+  free((void *)jb.ord);
+  return OK;
+}
+
+/* appearance.py:107-134 eval_fields: density and density-weighted radiance
+   of the mixture at x (direction d) over `active` (storage indices, NULL =
+   all), visited in ascending uid; zero density gives black. */
+int oracle_eval_fields(void *h, const double *x, const double *d, const int64_t *active,
+                       int64_t n_active, double *sigma_out, double *color_out) {
+  const oscene *s = (const oscene *)h;
+  int64_t *ord;
+  int64_t na;
+  if (active) {
+    na = n_active;
+    ord = malloc(sizeof(int64_t) * (na > 0 ? na : 1));
+    memcpy(ord, active, sizeof(int64_t) * na);
+    /* stable sort by uid (insertion: the lists are short) */
+    for (int64_t a = 1; a < na; ++a) {
+      const int64_t v = ord[a];
+      int64_t b = a;
+      while (b > 0 && s->uids[ord[b - 1]] > s->uids[v]) { ord[b] = ord[b - 1]; --b; }
+      ord[b] = v;
+    }
+  } else {
+    na = s->n;
+    ord = uid_order(s);
+  }
+  double sigma = 0.0, wsum[3] = {0, 0, 0};
+  for (int64_t a = 0; a < na; ++a) {
+    const int64_t i = ord[a];
+    if (i < 0 || i >= s->n) { free(ord); return ERR_ARG; }
+    const double *M = s->iso_inv + 9 * i, *mu = s->means + 3 * i;
+    double v[3], y[3];
+    for (int k = 0; k < 3; ++k) v[k] = x[k] - mu[k];
+    for (int b = 0; b < 3; ++b) y[b] = M[3 * b] * v[0] + M[3 * b + 1] * v[1] + M[3 * b + 2] * v[2];
+    const double q = y[0] * y[0] + y[1] * y[1] + y[2] * y[2];
+    if (q > 1.0) continue;
+    const double dens = s->sigmas[i] * exp(-0.5 * s->log_ratio[i] * q);
+    double c[3];
+    eval_radiance(s->coeffs + NCOEF * i, d, c, NULL, NULL);
+    sigma += dens;
+    for (int k = 0; k < 3; ++k) wsum[k] = wsum[k] + dens * c[k];
+  }
+  free(ord);
+  *sigma_out = sigma;
+  for (int k = 0; k < 3; ++k) color_out[k] = sigma == 0.0 ? 0.0 : wsum[k] / sigma;
+  return OK;
+}
+
 /* renderer.py:135-145 Camera.ray for every pixel (row py, col px), R is the
    camera-to-world rotation (row-major).  rays out: H*W*8. */
 void oracle_camera_rays(const double *center, const double *R, double focal, int64_t W,

@@ -13,7 +13,7 @@ import os
 import subprocess
 from pathlib import Path
 
-from .errors import BufferOverflow, EmptyScene, GsrayError, ValidationError
+from .errors import BufferOverflow, EmptyScene, GsrayError, TraversalOverflow, ValidationError
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libgsx.so"
@@ -113,6 +113,8 @@ _SIGS = {
     "gsx_densify_criteria": (INT, [P, P, P, I64, D, P, P, P]),
     "gsx_calibrate_fp32": (INT, [I64, P, P, P]),
     "gsx_calibrate_sfu": (INT, [I64, P, P, P]),
+    "gsx_reference_rays": (INT, [P, P, I64, P, I64, INT, D, P, P, P]),
+    "gsx_eval_fields": (INT, [P, P, I64, P, P, I64, P, I64, P, P, P, P]),
     "gsx_image_loss_workspace_bytes": (SZ, [I64, I64, I64]),
     "gsx_image_loss": (INT, [P, P, I64, I64, I64, D, P, P, P, P]),
     "gsx_iso_loss": (INT, [P, I64, D, D, P, P, P]),
@@ -174,6 +176,8 @@ def check(rc: int, what: str = ""):
         raise ValueError(f"{what}: {msg}")
     if rc == GSX_ERR_VALIDATION:
         raise ValidationError(f"{what}: {msg}")
+    if rc == GSX_ERR_STACK:
+        raise TraversalOverflow(f"{what}: {msg}")
     raise GsrayError(f"{what}: {msg} (status {rc})")
 
 
@@ -194,4 +198,6 @@ def raise_status(st, what: str = ""):
         raise BufferOverflow(count, cap)
     if code == GSX_ERR_ARG:
         raise ValueError(f"{what}: argument out of range at {index}")
+    if code == GSX_ERR_STACK:
+        raise TraversalOverflow(f"{what}: traversal stack overflow (pixel / ray {index})", index)
     check(code, what)

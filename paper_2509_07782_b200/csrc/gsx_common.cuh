@@ -118,6 +118,7 @@ struct BvhView {
   float4* nodes;
   int32_t* parents;
   float4* nodes4;
+  gsx_dev_status* status;  // per launch (nullable): traversal-stack overflow reports
 };
 
 __host__ __device__ inline int64_t bvh_internal_count(int64_t n) { return n > 1 ? n - 1 : 1; }
@@ -130,6 +131,7 @@ __host__ __device__ inline BvhView bvh_view(void* arena, int64_t n) {
   v.nodes = (float4*)p;
   v.parents = (int32_t*)(p + a);
   v.nodes4 = (float4*)(p + a + b);
+  v.status = nullptr;
   return v;
 }
 

@@ -160,7 +160,7 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
     PH_END(3, ph_c)
   }
   if (STATS) cnt.visits += visits;
-  emptiness_tail<STATS>(sv, bv, r, want, seg, nonempty, cnt);
+  emptiness_tail<STATS>(sv, bv, r, want, seg, nonempty, cnt, sm.ovf);
   return nonempty;
 }
 
@@ -246,7 +246,9 @@ __device__ void render_warp_block(const SceneView& sv, const BvhView& bv, const 
   RayAccum acc;
   acc.init();
   LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
+  ovf_begin(sw);
   march_forward<STATS, SAVE, CONE>(sv, bv, r, hit, cfg, acc, cnt, sw, lw);
+  ovf_report(sw, bv, py * W + px);
   if (SAVE) log_finish(lw, log_nw);
   if (valid) {
     int64_t pix = py * W + px;
@@ -350,7 +352,7 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     }
   }
   Counters<false> cnt;
-  emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt);
+  emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt, sm.ovf);
   return nonempty;
 }
 
@@ -391,12 +393,14 @@ __global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
   const YSmem Yv{&sw.ylane[0][lane]};
   const int ns = (int)cfg.n_s;
   Counters<false> cnt;
+  ovf_begin(sw);
   march_warp<false, true>(sv, bv, r, hit, cfg, acc, cnt,
                           cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sw,
                           [&](const Seg& seg, bool want) {
                             return forward_segment_screened(sv, bv, r, want, seg, ns, Yv, acc,
                                                             sw, sc);
                           });
+  ovf_report(sw, bv, py * W + px);
   if (valid) {
     const int64_t pix = py * W + px;
     const float T = hit ? acc.transmittance() : 1.f;
@@ -542,7 +546,9 @@ __global__ void __launch_bounds__(256, 2) k_render_rays(SceneView sv, BvhView bv
   RayAccum acc;
   acc.init();
   LogWriter lw = log_writer(nullptr, 0);
+  ovf_begin(smem[threadIdx.x >> 5]);
   march_forward<STATS, false, false>(sv, bv, r, hit, cfg, acc, cnt, smem[threadIdx.x >> 5], lw);
+  ovf_report(smem[threadIdx.x >> 5], bv, i);
   if (valid) {
     float T = hit ? acc.transmittance() : 1.f;
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = acc.C[k] + T * (float)cfg.background[k];
@@ -646,7 +652,7 @@ extern "C" int gsx_render_forward(const void* scene_arena, const void* bvh_arena
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
   cudaStream_t s = (cudaStream_t)stream;
-  (void)dev_status;
+  bv.status = dev_status;
   if (stats)
     return launch_camera<true, false>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb,
                                       depth, trans, stats, nullptr, 0, s);
@@ -695,7 +701,7 @@ extern "C" int gsx_render_forward_logged(const void* scene_arena, const void* bv
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
   cudaStream_t s = (cudaStream_t)stream;
-  (void)dev_status;
+  bv.status = dev_status;
   k_log_init<<<1, 1, 0, s>>>((LogHeader*)log, (unsigned long long)log_bytes,
                              (unsigned)(8 * ntl), table);
   return launch_camera<false, true>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb, depth,
@@ -725,7 +731,7 @@ extern "C" int gsx_render_rays(const void* scene_arena, const void* bvh_arena, i
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
   cudaStream_t s = (cudaStream_t)stream;
-  (void)dev_status;
+  bv.status = dev_status;
   unsigned blocks = (unsigned)((m + 255) / 256);
   if (stats)
     k_render_rays<true><<<blocks, 256, 0, s>>>(sv, bv, rays, m, clip, *cfg, rgb, depth, trans,
@@ -748,7 +754,7 @@ extern "C" int gsx_render_rays_stats(const void* scene_arena, const void* bvh_ar
   if (m <= 0) return GSX_OK;
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
-  (void)dev_status;
+  bv.status = dev_status;
   k_render_rays<true><<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       sv, bv, rays, m, clip, *cfg, rgb, depth, trans, nullptr,
       (unsigned long long*)per_ray);

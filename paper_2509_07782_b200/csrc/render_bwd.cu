@@ -400,7 +400,7 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
       count = 0;
     }
   }
-  emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt);
+  emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt, sm.ovf);
   return nonempty;
 }
 
@@ -485,9 +485,11 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
   WarpSmem& sm = smem[threadIdx.x >> 5];
   float* wsm = red_smem + (threadIdx.x >> 5) * BWD_WARP_FLOATS;
   GradBatch gb{wsm, wsm + RED_FLOATS, 0};
+  ovf_begin(sm);
   march_warp<false>(sv, bv, r, hit, cfg, acc, cnt, GSX_SYNC_BWD, sm, [&](const Seg& seg, bool want) {
     return backward_segment(sv, bv, r, want, seg, ns, Y, acc, pg, cnt, sm, gb, grad);
   });
+  ovf_report(sm, bv, pix);
   grad_batch_flush(sv, gb, grad);
 }
 
@@ -649,7 +651,6 @@ extern "C" int gsx_render_backward(const void* scene_arena, const void* bvh_aren
                                    const float* dL_ddepth, const float* dL_dtrans, float* grad,
                                    gsx_dev_status* dev_status, void* stream) {
   (void)params;
-  (void)dev_status;
   const BwdImages im{rgb, depth, trans, dL_drgb, dL_ddepth, dL_dtrans};
   int rc = bwd_check(cfg, cam, n, im, grad, tile_begin, tile_stride);
   if (rc) return rc;
@@ -658,6 +659,7 @@ extern "C" int gsx_render_backward(const void* scene_arena, const void* bvh_aren
   int64_t blocks = BWD_PER_TILE * ((tiles - tile_begin + tile_stride - 1) / tile_stride);
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
+  bv.status = dev_status;
   rc = bwd_smem_setup();
   if (rc) return rc;
   k_render_backward<<<(unsigned)blocks, BWD_THREADS, BWD_SMEM, (cudaStream_t)stream>>>(
@@ -674,7 +676,6 @@ extern "C" int gsx_render_backward_logged(const void* scene_arena, const void* b
                                           const float* dL_dtrans, const void* log, float* grad,
                                           gsx_dev_status* dev_status, void* stream) {
   (void)params;
-  (void)dev_status;
   const BwdImages im{rgb, depth, trans, dL_drgb, dL_ddepth, dL_dtrans};
   int rc = bwd_check(cfg, cam, n, im, grad, tile_begin, tile_stride);
   if (rc) return rc;
@@ -685,6 +686,7 @@ extern "C" int gsx_render_backward_logged(const void* scene_arena, const void* b
   const long long nw = 8 * ntl;
   SceneView sv = scene_view((void*)scene_arena, n);
   BvhView bv = bvh_view((void*)bvh_arena, n);
+  bv.status = dev_status;
   cudaStream_t s = (cudaStream_t)stream;
   rc = bwd_smem_setup();
   if (rc) return rc;

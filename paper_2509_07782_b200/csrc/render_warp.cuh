@@ -80,6 +80,7 @@ struct Counters {
 struct WarpSmem {
   int32_t stack[WSTACK];
   int32_t list[LCAP];
+  int ovf;  // a traversal stack of this warp overflowed (reported as GSX_ERR_STACK)
   float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | dlo | dhi)
 #if GSX_Y_SMEM
   float ylane[9][32];  // per-lane SH basis (forward)
@@ -153,6 +154,7 @@ __device__ inline void warp_traverse(const BvhView& bv, const RayCtx& r, bool wa
       st.overflow |= push && !fits;
       next = (inner && next < 0) ? c : next;
     }
+    if (st.overflow) sm.ovf = 1;
     __syncwarp();
     if (next < 0) {
       if (st.sp == 0) {
@@ -369,6 +371,7 @@ __device__ inline void warp_traverse_cone(const BvhView& bv, ConeTrav& st, WarpS
       sts_i_if(a_stack + 4u * (unsigned)pos, ch, inner && pos < WSTACK);
       count += __popc(bl);
       const int np = sp + __popc(bi);
+      if (np > WSTACK) sm.ovf = 1;  // dropped subtrees: the frame is flagged
       sp = np < WSTACK ? np : WSTACK;
     }
     st.sp = sp;
@@ -503,6 +506,8 @@ __device__ inline bool warp_closest_hit(const SceneView& sv, const BvhView& bv, 
       if (next >= 0 && sp < WSTACK) {
         asm volatile("st.shared.b32 [%0], %1;" ::"r"(a_stack + 4u * sp), "r"(next) : "memory");
         ++sp;
+      } else if (next >= 0) {
+        sm.ovf = 1;
       }
       next = ch[k];
     }
@@ -591,6 +596,18 @@ __device__ inline bool warp_closest_hit_cone(const SceneView& sv, const BvhView&
     return true;
   }
   return false;
+}
+
+// Traversal-stack overflow bookkeeping of one warp: cleared at the start of
+// the warp's work, reported once at the end (GSX_ERR_STACK with the pixel /
+// ray index of lane 0) through the launch's status word.
+__device__ inline void ovf_begin(WarpSmem& sm) {
+  if ((threadIdx.x & 31) == 0) sm.ovf = 0;
+  __syncwarp();
+}
+__device__ inline void ovf_report(const WarpSmem& sm, const BvhView& bv, int64_t index) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0 && sm.ovf) dev_fail(bv.status, GSX_ERR_STACK, index);
 }
 
 // per-lane description of the segment processed in this warp iteration
@@ -902,7 +919,7 @@ __device__ inline void accumulate_screened(const SceneView& sv, const RayCtx& r,
 template <bool STATS>
 static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhView& bv, const RayCtx& r,
                                       bool want, const Seg& seg, bool& nonempty,
-                                      Counters<STATS>& cnt) {
+                                      Counters<STATS>& cnt, int& sm_ovf) {
   PH_BEGIN(ph_ph)
   if (STATS) {
     if (want) {
@@ -918,7 +935,7 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
           }
           return false;
         };
-        traverse_segment<true>(bv, r, (float)a, (float)b, fn, v2);
+        if (!traverse_segment<true>(bv, r, (float)a, (float)b, fn, v2)) sm_ovf = 1;
       };
       // _collect_split (renderer.py:361-393): a collect of more than
       // buffer_capacity boxes splits the segment at its midpoint (samples
@@ -966,7 +983,7 @@ static __device__ GSX_COLD void emptiness_tail(const SceneView& sv, const BvhVie
       if (exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
       return nonempty;
     };
-    traverse_segment<true>(bv, r, (float)seg.t0, (float)seg.t1, probe, v2);
+    if (!traverse_segment<true>(bv, r, (float)seg.t0, (float)seg.t1, probe, v2)) sm_ovf = 1;
   }
   PH_END(4, ph_ph)
 }

@@ -105,7 +105,8 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
                                           ctypes.byref(cam_c), ctypes.byref(cfg_c),
                                           int(tile_begin), int(tile_stride), ptr(rgb),
                                           ptr(depth), ptr(trans), ptr(log.arena), log.capacity,
-                                          None, stream_ptr(stream)), "render_forward_logged")
+                                          ptr(scene.render_status()), stream_ptr(stream)),
+              "render_forward_logged")
         return rgb, depth, trans, None
     ws = None
     if screen and not stats:
@@ -113,8 +114,8 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
     check(L.gsx_render_forward(ptr(scene.arena), ptr(scene.bvh_arena), scene.n,
                                ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
                                int(tile_stride), ptr(rgb), ptr(depth), ptr(trans), ptr(st),
-                               ptr(ws), 0 if ws is None else ws.numel(), None,
-                               stream_ptr(stream)), "render_forward")
+                               ptr(ws), 0 if ws is None else ws.numel(),
+                               ptr(scene.render_status()), stream_ptr(stream)), "render_forward")
     return rgb, depth, trans, st
 
 
@@ -141,14 +142,15 @@ def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans,
             ptr(scene.arena), ptr(scene.bvh_arena), ptr(scene.params), scene.n,
             ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin), int(tile_stride),
             ptr(c(rgb)), ptr(c(depth)), ptr(c(trans)), ptr(c(dL_drgb)), ptr(c(dL_ddepth)),
-            ptr(c(dL_dtrans)), ptr(log.arena), ptr(grad), None, stream_ptr(stream)),
-            "render_backward_logged")
+            ptr(c(dL_dtrans)), ptr(log.arena), ptr(grad), ptr(scene.render_status()),
+            stream_ptr(stream)), "render_backward_logged")
         return grad
     check(L.gsx_render_backward(ptr(scene.arena), ptr(scene.bvh_arena), ptr(scene.params), scene.n,
                                 ctypes.byref(cam_c), ctypes.byref(cfg_c), int(tile_begin),
                                 int(tile_stride), ptr(c(rgb)), ptr(c(depth)), ptr(c(trans)),
                                 ptr(c(dL_drgb)), ptr(c(dL_ddepth)), ptr(c(dL_dtrans)), ptr(grad),
-                                None, stream_ptr(stream)), "render_backward")
+                                ptr(scene.render_status()), stream_ptr(stream)),
+          "render_backward")
     return grad
 
 
@@ -168,20 +170,32 @@ def lazy_stats(scene, camera: Camera, cfg: RenderConfig) -> LazyRenderStats:
     return LazyRenderStats(compute)
 
 
+def to_host64(t) -> np.ndarray:
+    """float64 host copy of a float32 CUDA tensor: widened on the device, then
+    one DMA into page-locked memory (torch's caching host allocator recycles
+    the block once the returned array is gone)."""
+    out = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+    out.copy_(t.double())
+    return out.numpy()
+
+
 def render_image(scene, camera: Camera, cfg: RenderConfig, threads: int | None = None):
     """renderer.py:396-437: returns (image (H,W,3) float64 numpy, RenderStats).
     `threads` / GSRAY_THREADS are accepted and ignored (one CUDA thread per ray).
     The image comes from the plain (screened) forward; the RenderStats are
     lazy: reading a counter runs the exact-counter pass then."""
     rgb, _, _, _ = render(scene, camera, cfg)
-    return rgb.double().cpu().numpy(), lazy_stats(scene, camera, cfg)
+    img = to_host64(rgb)
+    scene.check_render_status()
+    return img, lazy_stats(scene, camera, cfg)
 
 
 def render_full(scene, camera: Camera, cfg: RenderConfig):
     """(rgb, depth, trans) as float64 numpy plus (lazy) RenderStats."""
     rgb, depth, trans, _ = render(scene, camera, cfg)
-    return (rgb.double().cpu().numpy(), depth.double().cpu().numpy(),
-            trans.double().cpu().numpy(), lazy_stats(scene, camera, cfg))
+    out = (to_host64(rgb), to_host64(depth), to_host64(trans))
+    scene.check_render_status()
+    return out + (lazy_stats(scene, camera, cfg),)
 
 
 def march_rays(scene, rays, cfg: RenderConfig, clip: bool = False, stats: bool = False):
@@ -202,8 +216,10 @@ def march_rays(scene, rays, cfg: RenderConfig, clip: bool = False, stats: bool =
     cfg_c = cfg.to_c()
     check(L.gsx_render_rays(ptr(scene.arena), ptr(scene.bvh_arena), scene.n, ptr(r), m,
                             int(bool(clip)), ctypes.byref(cfg_c), ptr(rgb), ptr(depth),
-                            ptr(trans), ptr(st), None, stream_ptr()), "render_rays")
+                            ptr(trans), ptr(st), ptr(scene.render_status()), stream_ptr()),
+          "render_rays")
     s = RenderStats.from_counts(st.cpu().numpy()) if stats else None
+    scene.check_render_status()
     return (rgb.cpu().numpy().astype(np.float64), depth.cpu().numpy().astype(np.float64),
             trans.cpu().numpy().astype(np.float64), s)
 
@@ -224,8 +240,11 @@ def ray_stats(scene, rays, cfg: RenderConfig, clip: bool = False):
     cfg_c = cfg.to_c()
     check(L.gsx_render_rays_stats(ptr(scene.arena), ptr(scene.bvh_arena), scene.n, ptr(r), m,
                                   int(bool(clip)), ctypes.byref(cfg_c), ptr(rgb), None, None,
-                                  ptr(per), None, stream_ptr()), "render_rays_stats")
-    return per.cpu().numpy()
+                                  ptr(per), ptr(scene.render_status()), stream_ptr()),
+          "render_rays_stats")
+    out = per.cpu().numpy()
+    scene.check_render_status()
+    return out
 
 
 def march_ray(scene, ray: Ray, cfg: RenderConfig, stats: RenderStats | None = None):
@@ -259,6 +278,38 @@ def clip_ray_to_scene(scene, ray: Ray) -> Ray | None:
     if t0 >= t1:
         return None
     return Ray(ray.origin, ray.direction, t0, t1)
+
+
+def reference_rays(scene, rays, fine_dt: float, background=(0.0, 0.0, 0.0),
+                   clip: bool = False) -> np.ndarray:
+    """Dense all-primitive quadrature of a batch of rays [M,8] (o, d, t_near,
+    t_far) on the device, float64 (gsx_reference_rays): reference_integrate
+    per ray, after clip_ray_to_scene when `clip` (reference_render)."""
+    import ctypes
+
+    L = _lib.lib()
+    dev = scene.device
+    r = torch.as_tensor(np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 8), device=dev)
+    bg = (ctypes.c_double * 3)(*[float(v) for v in background])
+    out = torch.empty((r.shape[0], 3), dtype=torch.float64, device=dev)
+    check(L.gsx_reference_rays(ptr(scene.arena), ptr(scene.params), scene.n, ptr(r), r.shape[0],
+                               int(bool(clip)), float(fine_dt), bg, ptr(out), stream_ptr()),
+          "reference_rays")
+    return out.cpu().numpy()
+
+
+def reference_integrate(scene, ray: Ray, fine_dt: float, background=(0.0, 0.0, 0.0)):
+    """renderer.py:440-480: dense uniform quadrature of one ray over its
+    [t_near, t_far] against every primitive (no BVH, no skipping) -- the
+    oracle the renderer's tests compare against.  Returns rgb (3,) float64."""
+    return reference_rays(scene, ray.as_array()[None], fine_dt, background, clip=False)[0]
+
+
+def reference_render(scene, camera: Camera, fine_dt: float, background=(0.0, 0.0, 0.0)):
+    """renderer.py:483-493: reference_integrate per pixel with render_image's
+    ray clipping; (H,W,3) float64."""
+    img = reference_rays(scene, camera.rays(), fine_dt, background, clip=True)
+    return img.reshape(camera.height, camera.width, 3)
 
 
 def psnr(a, b, data_range: float = 1.0) -> float:

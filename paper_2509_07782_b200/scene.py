@@ -95,6 +95,26 @@ class Scene:
         self.bounds_t = torch.empty(6, dtype=torch.float64, device=dev)
         self._status = _lib.new_status(dev)
 
+    def render_status(self):
+        """Sticky device status word of this scene's renders (traversal-stack
+        overflow, GSX_ERR_STACK): written by the kernels, read -- and the
+        error raised -- only by check_render_status(), so renders stay
+        asynchronous."""
+        st = getattr(self, "_render_st", None)
+        if st is None:
+            st = _lib.new_status(self.device)
+            self._render_st = st
+        return st
+
+    def check_render_status(self):
+        """Raise TraversalOverflow if any render / backward of this scene since
+        the last check overflowed a traversal stack (synchronizes), then clear."""
+        st = self.render_status()
+        try:
+            _lib.raise_status(st, "render")
+        finally:
+            st.copy_(_lib.new_status(self.device))
+
     def render_workspace(self):
         """The scene's default per-render workspace (gsx_render_workspace_bytes:
         the per-camera silhouette table of the screened forward)."""

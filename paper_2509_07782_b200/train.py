@@ -298,6 +298,7 @@ class Trainer:
         if self.log is not None and (self._steps == 1 or want_loss):
             self.log.ensure()  # overflowed warps were replayed; size up for the next step
         if want_loss:
+            s.check_render_status()  # a traversal-stack overflow since the last check
             iso = float(self._iso.item()) / s.n if self.rank == 0 else 0.0
             return vals[0] + self.iso_cfg.lambda_s * iso
         return None
