@@ -181,7 +181,7 @@ def test_deep_tree_traversals_agree():
         b = G.render(scene, cam, cfg, screen=False, traversal=1)[0].cpu().numpy()
         c = G.render(scene, cam, cfg, screen=False, traversal=2)[0].cpu().numpy()
         scene.check_render_status()
-        assert np.array_equal(a, b)
+        assert np.abs(a - b).max() < 2e-6  # same arithmetic, other fp32 contraction
         assert np.abs(a - c).max() < 2e-5
         rays = O.camera_rays(cam.center, cam.quat, cam.focal, cam.width, cam.height)
         sel = np.arange(0, cam.width * cam.height, 7)
