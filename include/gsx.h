@@ -270,13 +270,15 @@ int gsx_render_backward(const void* scene_arena, const void* bvh_arena, const fl
  * gsx_render_backward_logged, so any capacity >= gsx_march_log_min_bytes is
  * correct; gsx_march_log_usage (synchronizes `stream`) reports the bytes the
  * last forward needed and whether it overflowed.  The backward must use the
- * same camera, cfg, tiles and scene as the logged forward. */
+ * same camera, cfg, tiles and scene as the logged forward.  ws / ws_bytes:
+ * as gsx_render_forward (nullable; with it the logged forward is the
+ * silhouette-screened kernel too). */
 int64_t gsx_march_log_min_bytes(const gsx_camera* cam, int64_t tile_begin, int64_t tile_stride);
 int gsx_render_forward_logged(const void* scene_arena, const void* bvh_arena, int64_t n,
                               const gsx_camera* cam, const gsx_render_cfg* cfg,
                               int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
-                              float* trans, void* log, int64_t log_bytes,
-                              gsx_dev_status* dev_status, void* stream);
+                              float* trans, void* log, int64_t log_bytes, void* ws,
+                              int64_t ws_bytes, gsx_dev_status* dev_status, void* stream);
 int gsx_render_backward_logged(const void* scene_arena, const void* bvh_arena,
                                const float* params, int64_t n, const gsx_camera* cam,
                                const gsx_render_cfg* cfg, int64_t tile_begin, int64_t tile_stride,

@@ -104,7 +104,8 @@ _SIGS = {
     "gsx_render_rays_stats": (INT, [P, P, I64, P, I64, INT, P, P, P, P, P, P, P]),
     "gsx_render_backward": (INT, [P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, P, P, P]),
     "gsx_march_log_min_bytes": (I64, [P, I64, I64]),
-    "gsx_render_forward_logged": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, I64, P, P]),
+    "gsx_render_forward_logged": (INT, [P, P, I64, P, P, I64, I64, P, P, P, P, I64, P, I64, P,
+                                        P]),
     "gsx_render_backward_logged": (INT, [P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, P, P,
                                          P, P]),
     "gsx_march_log_usage": (INT, [P, P, P, P]),

@@ -211,6 +211,19 @@ __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, do
   }
 }
 
+// kind 0 from per-sample sums held in a shared-memory column (the screened
+// forward's acc[j][lane], stride 32 float4)
+__device__ inline void log_full_col(LogWriter& w, const int32_t* list, int count, double tb,
+                                    double dt, int mc, const float4* col) {
+  if (!w.base) return;
+  int nact, mmax;
+  float4* smp = log_full_head(w, list, count, tb, dt, mc, nact, mmax);
+  if (smp) {
+    for (int j = 0; j < mmax; ++j)
+      __stcs(smp + (long long)j * nact, j < mc ? col[32 * j] : make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+}
+
 // end of the warp: publish its chain head and whether it is complete
 __device__ inline void log_finish(const LogWriter& w, long long nw) {
   if (!w.base || (threadIdx.x & 31) != 0) return;

@@ -291,10 +291,11 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
 // march, same per-lane arithmetic in the same order: its pixels equal the
 // unscreened kernel's bit for bit.
 // ---------------------------------------------------------------------------
-template <class YT>
+template <bool SAVE, class YT>
 __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
                                          const RayCtx& r, bool want, const Seg& seg, int ns,
-                                         YT Y, RayAccum& acc, WarpSmemS& sm, const Screen& sc) {
+                                         YT Y, RayAccum& acc, WarpSmemS& sm, const Screen& sc,
+                                         LogWriter& lw) {
   constexpr int CH = GSX_SCR_CH;
   bool nonempty = false;
   const float dtf = (float)seg.dt;
@@ -324,12 +325,13 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     ConeTrav cst;
     cone_begin(sm, cst);
     const unsigned lanes = __ballot_sync(FULL, wch && mc > 0);
-    int count = 0;
+    const bool save = SAVE && __any_sync(FULL, want && mc > 0);
+    int count = 0, kept = 0;
     for (;;) {
       warp_traverse_cone(bv, cst, sm, count, visits);
       screen_list(sc, sm, count, lanes);
       bool inside = false;
-      accumulate_screened<CH>(sv, r, sm, count, wch, mc, base, dtf, Y, inside);
+      kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, inside);
       nonempty = nonempty || inside;
       // AABB emptiness without a clearly-inside sample: the exact test over
       // this chunk of the list (a superset of the boxes the segment meets)
@@ -341,7 +343,12 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
           }
       __syncwarp();
       if (cst.done) break;
+      if (save) log_list_chunk(lw, (const int32_t*)sm.mask, kept);
+      __syncwarp();
       count = 0;
+    }
+    if constexpr (SAVE) {
+      if (save) log_full_col(lw, (const int32_t*)sm.mask, kept, tb, seg.dt, mc, col);
     }
     // front-to-back compositing (renderer.py:230-239)
 #pragma unroll
@@ -359,14 +366,20 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
 #ifndef GSX_SCR_THREADS
 #define GSX_SCR_THREADS 32
 #endif
+#ifndef GSX_SCR_YSMEM
+#define GSX_SCR_YSMEM 1
+#endif
+#ifndef GSX_SCR_THREADS_LOGGED  // CTA of the screened training forward
+#define GSX_SCR_THREADS_LOGGED 64
+#endif
 #ifndef GSX_SCR_MINB  // CTAs of 32 threads per SM (registers: 65536 / (32 MINB))
 #define GSX_SCR_MINB 16
 #endif
-template <int NT>
+template <int NT, bool SAVE>
 __global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
     k_render_screened(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
                       int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
-                      float* trans, const float4* view) {
+                      float* trans, const float4* view, void* log, long long log_nw) {
   __shared__ WarpSmemS smem[NT / 32];
   WarpSmemS& sw = smem[threadIdx.x >> 5];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
@@ -387,19 +400,25 @@ __global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
   const Screen sc{view, (float)((tile % tiles_x) * 16 + bx), (float)((tile / tiles_x) * 16 + by)};
   float Y[9];
   sh_basis_f(r.df, Y);
+#if GSX_SCR_YSMEM
 #pragma unroll
   for (int b = 0; b < 9; ++b) sw.ylane[b][lane] = Y[b];
   __syncwarp();
   const YSmem Yv{&sw.ylane[0][lane]};
+#else
+  const float* Yv = Y;  // (128 registers: the basis stays in registers)
+#endif
   const int ns = (int)cfg.n_s;
   Counters<false> cnt;
+  LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
   ovf_begin(sw);
   march_warp<false, true>(sv, bv, r, hit, cfg, acc, cnt,
                           cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sw,
                           [&](const Seg& seg, bool want) {
-                            return forward_segment_screened(sv, bv, r, want, seg, ns, Yv, acc,
-                                                            sw, sc);
+                            return forward_segment_screened<SAVE>(sv, bv, r, want, seg, ns, Yv,
+                                                                  acc, sw, sc, lw);
                           });
+  if (SAVE) log_finish(lw, log_nw);
   ovf_report(sw, bv, py * W + px);
   if (valid) {
     const int64_t pix = py * W + px;
@@ -447,14 +466,23 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
   if constexpr (!SAVE && !STATS) {
     if (view && FWD_CONE(false)) {
       const long long ctas = 8 * (long long)ntl / (GSX_SCR_THREADS / 32);
-      k_render_screened<GSX_SCR_THREADS><<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(
-          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view);
+      k_render_screened<GSX_SCR_THREADS, false><<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(
+          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, nullptr, 0);
       return gsx_check_launch();
     }
     if (tile_stride == 1)
       return launch_camera_nt<STATS, SAVE, GSX_FWD_THREADS_WHOLE>(
           sv, bv, cam, cfg, tile_begin, tile_stride, ntl, rgb, depth, trans, stats, log, log_nw,
           s);
+  }
+  if constexpr (SAVE && !STATS) {
+    if (view && FWD_CONE(true)) {  // screened logged (training) forward
+      constexpr int NT = GSX_SCR_THREADS_LOGGED;
+      const long long ctas = 8 * (long long)ntl / (NT / 32);
+      k_render_screened<NT, true><<<(unsigned)ctas, NT, 0, s>>>(
+          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, log, log_nw);
+      return gsx_check_launch();
+    }
   }
   return launch_camera_nt<STATS, SAVE, FWD_THREADS>(sv, bv, cam, cfg, tile_begin, tile_stride,
                                                     ntl, rgb, depth, trans, stats, log, log_nw,
@@ -686,8 +714,9 @@ extern "C" int gsx_render_forward_logged(const void* scene_arena, const void* bv
                                          int64_t n, const gsx_camera* cam,
                                          const gsx_render_cfg* cfg, int64_t tile_begin,
                                          int64_t tile_stride, float* rgb, float* depth,
-                                         float* trans, void* log, int64_t log_bytes,
-                                         gsx_dev_status* dev_status, void* stream) {
+                                         float* trans, void* log, int64_t log_bytes, void* ws,
+                                         int64_t ws_bytes, gsx_dev_status* dev_status,
+                                         void* stream) {
   int rc = gsx_validate_cfg(cfg);
   if (rc) return rc;
   if (!cam || cam->width < 1 || cam->height < 1 || !(cam->focal > 0)) return GSX_ERR_ARG;
@@ -704,8 +733,14 @@ extern "C" int gsx_render_forward_logged(const void* scene_arena, const void* bv
   bv.status = dev_status;
   k_log_init<<<1, 1, 0, s>>>((LogHeader*)log, (unsigned long long)log_bytes,
                              (unsigned)(8 * ntl), table);
+  float4* view = nullptr;
+  if (ws) {
+    if (ws_bytes < (int64_t)gsx_render_workspace_bytes(n)) return GSX_ERR_ARG;
+    view = (float4*)ws;
+    k_view_conics<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sv, n, *cam, view);
+  }
   return launch_camera<false, true>(sv, bv, *cam, *cfg, tile_begin, tile_stride, ntl, rgb, depth,
-                                    trans, nullptr, log, 8 * ntl, s);
+                                    trans, nullptr, log, 8 * ntl, s, view);
 }
 
 extern "C" int gsx_march_log_usage(const void* log, int64_t* used_bytes, int* overflow,

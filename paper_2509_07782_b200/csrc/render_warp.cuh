@@ -841,10 +841,15 @@ __device__ inline void screen_list(const Screen& sc, WarpSmemS& sm, int count, u
 // clearly inside an ellipsoid (q <= 0.998 in fp32): that sample is then
 // inside the primitive's fp64 AABB too, so the segment is AABB-non-empty in
 // the reference's sense (spatial.py:234-241) without the exact slab test.
-template <int CH, class YT>
-__device__ inline void accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemS& sm,
-                                           int count, bool want, int mc, const SegBase& base,
-                                           float dtf, YT Y, bool& inside) {
+// COMPACT (logged forward): the entries some lane used -- the only ones the
+// logged backward needs -- are also written, in list order, over the
+// already-consumed front of sm.mask (read back as int32); returns their
+// count.  sm.list stays whole for the exact emptiness test.
+template <int CH, bool COMPACT = false, class YT>
+__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemS& sm,
+                                          int count, bool want, int mc, const SegBase& base,
+                                          float dtf, YT Y, bool& inside) {
+  int kept = 0;
   const unsigned lane = threadIdx.x & 31;
   float4* col = &sm.acc[0][lane];
 #if GSX_SCR_PREF
@@ -876,6 +881,10 @@ __device__ inline void accumulate_screened(const SceneView& sv, const RayCtx& r,
 #endif
     CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
     if (!__any_sync(FULL, u.use)) continue;
+    if (COMPACT) {
+      if (lane == 0) sm.mask[kept] = (uint32_t)p;  // kept <= i: masks ahead are intact
+      ++kept;
+    }
     const CandSetup& cs = u.cs;
     float c[3] = {0.f, 0.f, 0.f};
     if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
@@ -912,6 +921,8 @@ __device__ inline void accumulate_screened(const SceneView& sv, const RayCtx& r,
 #endif
     inside = inside || qmn <= 0.998f;
   }
+  if (COMPACT) __syncwarp();
+  return COMPACT ? kept : count;
 }
 
 // Exact AABB-emptiness of the lane's segment (reference semantics) after the

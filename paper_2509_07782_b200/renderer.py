@@ -101,10 +101,14 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
             raise ValueError("stats and log are exclusive")
         if (log.tile_begin, log.tile_stride) != (int(tile_begin), int(tile_stride)):
             raise ValueError("march log was sized for another tile set")
+        ws = None
+        if screen:
+            ws = workspace if workspace is not None else scene.render_workspace()
         check(L.gsx_render_forward_logged(ptr(scene.arena), ptr(scene.bvh_arena), scene.n,
                                           ctypes.byref(cam_c), ctypes.byref(cfg_c),
                                           int(tile_begin), int(tile_stride), ptr(rgb),
                                           ptr(depth), ptr(trans), ptr(log.arena), log.capacity,
+                                          ptr(ws), 0 if ws is None else ws.numel(),
                                           ptr(scene.render_status()), stream_ptr(stream)),
               "render_forward_logged")
         return rgb, depth, trans, None
