@@ -99,6 +99,10 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world:
     scene = G.Scene.from_records(jit.astype(np.float32))
     del tscene
     tr = Trainer(scene, cam, cfg)
+    tr.step(target)  # sizes the march log
+    from paper_2509_07782_b200.renderer import autotune
+
+    tuned = autotune(scene, cam, cfg, log=tr.log, tile_begin=tr.rank, tile_stride=tr.world)
     for _ in range(warmup):
         tr.step(target)
     torch.cuda.synchronize()
@@ -122,6 +126,7 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world:
         ms = float(t.item())
     l1 = tr.step(target, want_loss=True)
     out = {"workload": desc, "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "forward_kernel": tuned,
            "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
            "rays_per_step": cam_kw["width"] * cam_kw["height"], "n_gpus": world}
     if world > 1:  # the phase breakdown below is a single-GPU, full-frame measurement
@@ -465,6 +470,18 @@ def main():
         if world > 1:
             gather_tiles(list(out), cam.width, cam.height)
 
+    # pick the forward kernel for this device and workload (renderer.VARIANTS,
+    # identical pixels): device-event timing of each once, before the warm-up
+    from paper_2509_07782_b200.renderer import VARIANTS, autotune
+
+    tuned = autotune(scene, cam, cfg, tile_begin=tb, tile_stride=ts)
+    if world > 1:  # every rank runs the same kernel (rank 0's choice)
+        choice = torch.tensor([list(VARIANTS).index(tuned["best"])], device=dev)
+        dist.broadcast(choice, 0)
+        tuned["best"] = list(VARIANTS)[int(choice.item())]
+        from paper_2509_07782_b200 import renderer as _r
+
+        _r._TUNED[_r._tune_key(scene, cam, cfg, False, ts)] = tuned["best"]
     with ClockSampler(local_rank) as clk:
         for _ in range(args.warmup):
             step()
@@ -503,7 +520,8 @@ def main():
     cs = torch.cuda.Stream(device=dev)
     rendered = [torch.cuda.Event() for _ in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
-    ws = scene.render_workspace()
+    screen_e2e, sums_e2e = VARIANTS[tuned["best"]]
+    ws = scene.render_workspace() if screen_e2e else None
 
     def e2e_frames(n):
         for k in range(n):
@@ -511,11 +529,12 @@ def main():
             if k >= 2:
                 s.wait_event(copied[b])
             flush.zero_()
-            cam_c, cfg_c = cam.to_c(), cfg.to_c()  # host structs, by pointer
+            cam_c, cfg_c = cam.to_c(), cfg.to_c(0, sums_e2e)  # host structs, by pointer
             _lib.check(L.gsx_render_forward(
                 _lib.ptr(scene.arena), _lib.ptr(scene.bvh_arena), scene.n, ctypes.byref(cam_c),
                 ctypes.byref(cfg_c), tb, ts, *(_lib.ptr(t) for t in devb[b]), None,
-                _lib.ptr(ws), ws.numel(), None, _lib.stream_ptr(s)), "render_forward")
+                _lib.ptr(ws), 0 if ws is None else ws.numel(), None, _lib.stream_ptr(s)),
+                "render_forward")
             if world > 1:
                 gather_tiles(devb[b], cam.width, cam.height)
             rendered[b].record(s)
@@ -601,8 +620,10 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "fps": 1e3 / ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config, "roofline": roof, "e2e": e2e,
-        "gpu_launches": 2 * args.steps, "gpu_launches_note": "k_view_conics + k_render_screened "
-        "per frame", "clocks": clk.summary(), "build_ms": build_ms, "setup_s": setup_s,
+        "gpu_launches": (2 if VARIANTS[tuned["best"]][0] else 1) * args.steps,
+        "gpu_launches_note": "per frame: k_view_conics + k_render_screened (screened variants) "
+        "or k_render_camera (plain)", "kernel": tuned,
+        "clocks": clk.summary(), "build_ms": build_ms, "setup_s": setup_s,
         "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
         "step_ms": step_ms,
     }

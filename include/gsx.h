@@ -65,6 +65,11 @@ typedef struct {
      renders, 0 = by focal length (packet cone for focal >= 1024 px), 1 =
      packet cone, 2 = per-lane packet.  Pixels do not depend on it. */
   int64_t traversal;
+  /* extension: per-sample sums of the screened camera forward (with a
+     workspace), 0 = shared memory (16 warps / SM, no spills), 1 = registers
+     (32 warps / SM).  Pixels do not depend on it; which is faster depends on
+     the device's memory latency (renderer.autotune picks per workload). */
+  int64_t sums;
 } gsx_render_cfg;
 
 /* Camera (renderer.py:109-145): camera-to-world rotation R (row-major, from the

@@ -14,8 +14,8 @@ from .densify import (DensifyConfig, GradAccumulator, criterion_new, criterion_o
                       neighbor_density, observe_scene)
 from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptyScene, GsrayError,
                      ParseError, TraversalOverflow, ValidationError)
-from .renderer import (MarchLog, clip_ray_to_scene, march_ray, march_rays, psnr,
-                       reference_integrate, reference_render, reference_rays, render,
+from .renderer import (VARIANTS, MarchLog, autotune, clip_ray_to_scene, march_ray, march_rays,
+                       psnr, reference_integrate, reference_render, reference_rays, render,
                        render_backward, render_full, render_image)
 from .scene import Scene, gen_test_scene, load_scene, reorder_by_morton, save_scene
 from .scene_io import (load_cameras, load_ply_scene, ply_records,
@@ -49,4 +49,5 @@ __all__ = [
     "criterion_old", "eval_fields_batch", "load_ply_scene", "look_at_camera", "march_rays",
     "neighbor_density", "observe_scene", "orbit_cameras", "ply_records", "quat_to_rotation",
     "reference_rays", "render", "render_backward", "render_full", "sh_basis", "TraversalOverflow",
+    "VARIANTS", "autotune",
 ]

@@ -211,16 +211,18 @@ __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, do
   }
 }
 
-// kind 0 from per-sample sums held in a shared-memory column (the screened
-// forward's acc[j][lane], stride 32 float4)
-__device__ inline void log_full_col(LogWriter& w, const int32_t* list, int count, double tb,
-                                    double dt, int mc, const float4* col) {
+// kind 0 from the screened forward's sums (sums.get(j) = (sigma_j, W_j))
+template <class Sums>
+__device__ inline void log_full_sums(LogWriter& w, const int32_t* list, int count, double tb,
+                                     double dt, int mc, const Sums& sums) {
   if (!w.base) return;
   int nact, mmax;
   float4* smp = log_full_head(w, list, count, tb, dt, mc, nact, mmax);
   if (smp) {
-    for (int j = 0; j < mmax; ++j)
-      __stcs(smp + (long long)j * nact, j < mc ? col[32 * j] : make_float4(0.f, 0.f, 0.f, 0.f));
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < mmax)
+        __stcs(smp + (long long)j * nact, j < mc ? sums.get(j) : make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 

@@ -64,6 +64,8 @@
 #define GSX_CONE_CH 1
 #endif
 #define FWD_CONE(save) (GSX_FWD_CONE == 1 || (GSX_FWD_CONE == 2 && !(save)))
+#include <type_traits>
+
 #include "gsx_common.cuh"
 #include "march_log.cuh"
 #include "render_warp.cuh"
@@ -291,16 +293,18 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
 // march, same per-lane arithmetic in the same order: its pixels equal the
 // unscreened kernel's bit for bit.
 // ---------------------------------------------------------------------------
-template <bool SAVE, class YT>
+template <bool SAVE, bool SMEM, class YT, class WS>
 __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
                                          const RayCtx& r, bool want, const Seg& seg, int ns,
-                                         YT Y, RayAccum& acc, WarpSmemS& sm, const Screen& sc,
+                                         YT Y, RayAccum& acc, WS& sm, const Screen& sc,
                                          LogWriter& lw) {
   constexpr int CH = GSX_SCR_CH;
   bool nonempty = false;
   const float dtf = (float)seg.dt;
   const int nchunks = (ns + CH - 1) / CH;
-  float4* col = &sm.acc[0][threadIdx.x & 31];
+  using Sums = std::conditional_t<SMEM, SmemSums, RegSums<CH>>;
+  Sums sums;
+  if constexpr (SMEM) sums.col = &sm.acc[0][threadIdx.x & 31];
   uint32_t visits = 0;
   for (int ch = 0; ch < nchunks; ++ch) {
     int mc = want ? seg.m - ch * CH : 0;
@@ -309,8 +313,7 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     if (!__any_sync(FULL, wch)) continue;
     const double tb = seg.tbase + (double)(ch * CH) * seg.dt;
     const SegBase base = seg_base(r, tb);
-#pragma unroll
-    for (int j = 0; j < CH; ++j) col[32 * j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sums.zero(CH);
     SegLimits lim;
     if (nchunks == 1) {
       lim = seg_limits(r, seg);
@@ -331,7 +334,8 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       warp_traverse_cone(bv, cst, sm, count, visits);
       screen_list(sc, sm, count, lanes);
       bool inside = false;
-      kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, inside);
+      kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sums,
+                                           inside);
       nonempty = nonempty || inside;
       // AABB emptiness without a clearly-inside sample: the exact test over
       // this chunk of the list (a superset of the boxes the segment meets)
@@ -348,12 +352,12 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       count = 0;
     }
     if constexpr (SAVE) {
-      if (save) log_full_col(lw, (const int32_t*)sm.mask, kept, tb, seg.dt, mc, col);
+      if (save) log_full_sums(lw, (const int32_t*)sm.mask, kept, tb, seg.dt, mc, sums);
     }
     // front-to-back compositing (renderer.py:230-239)
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
-      const float4 a = col[32 * j];
+      const float4 a = sums.get(j);
       const float w3[3] = {a.y, a.z, a.w};
       acc.add_sample(j < mc ? a.x : 0.f, w3, (float)(tb + (double)j * seg.dt), dtf);
     }
@@ -375,13 +379,20 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
 #ifndef GSX_SCR_MINB  // CTAs of 32 threads per SM (registers: 65536 / (32 MINB))
 #define GSX_SCR_MINB 16
 #endif
-template <int NT, bool SAVE>
-__global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
+#ifndef GSX_SCRR_MINB  // the same for the register-sum variant
+#define GSX_SCRR_MINB 32
+#endif
+
+// SMEM: per-sample sums in shared memory (16 warps / SM at 128 registers) or
+// in registers (32 warps / SM at 64 registers, sums spilled to local memory)
+template <int NT, bool SAVE, bool SMEM>
+__global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32 / NT)
     k_render_screened(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
                       int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
                       float* trans, const float4* view, void* log, long long log_nw) {
-  __shared__ WarpSmemS smem[NT / 32];
-  WarpSmemS& sw = smem[threadIdx.x >> 5];
+  using WS = std::conditional_t<SMEM, WarpSmemS, WarpSmemR>;
+  __shared__ WS smem[NT / 32];
+  WS& sw = smem[threadIdx.x >> 5];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   const int64_t W = cam.width, H = cam.height;
   const int64_t tiles_x = (W + 15) / 16;
@@ -415,8 +426,8 @@ __global__ void __launch_bounds__(NT, GSX_SCR_MINB * 32 / NT)
   march_warp<false, true>(sv, bv, r, hit, cfg, acc, cnt,
                           cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sw,
                           [&](const Seg& seg, bool want) {
-                            return forward_segment_screened<SAVE>(sv, bv, r, want, seg, ns, Yv,
-                                                                  acc, sw, sc, lw);
+                            return forward_segment_screened<SAVE, SMEM>(sv, bv, r, want, seg,
+                                                                        ns, Yv, acc, sw, sc, lw);
                           });
   if (SAVE) log_finish(lw, log_nw);
   ovf_report(sw, bv, py * W + px);
@@ -466,8 +477,14 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
   if constexpr (!SAVE && !STATS) {
     if (view && FWD_CONE(false)) {
       const long long ctas = 8 * (long long)ntl / (GSX_SCR_THREADS / 32);
-      k_render_screened<GSX_SCR_THREADS, false><<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(
-          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, nullptr, 0);
+      if (cfg.sums == 1)
+        k_render_screened<GSX_SCR_THREADS, false, false>
+            <<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(sv, bv, cam, cfg, tile_begin, tile_stride,
+                                                        rgb, depth, trans, view, nullptr, 0);
+      else
+        k_render_screened<GSX_SCR_THREADS, false, true>
+            <<<(unsigned)ctas, GSX_SCR_THREADS, 0, s>>>(sv, bv, cam, cfg, tile_begin, tile_stride,
+                                                        rgb, depth, trans, view, nullptr, 0);
       return gsx_check_launch();
     }
     if (tile_stride == 1)
@@ -479,8 +496,12 @@ int launch_camera(const SceneView& sv, const BvhView& bv, const gsx_camera& cam,
     if (view && FWD_CONE(true)) {  // screened logged (training) forward
       constexpr int NT = GSX_SCR_THREADS_LOGGED;
       const long long ctas = 8 * (long long)ntl / (NT / 32);
-      k_render_screened<NT, true><<<(unsigned)ctas, NT, 0, s>>>(
-          sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, log, log_nw);
+      if (cfg.sums == 1)
+        k_render_screened<NT, true, false><<<(unsigned)ctas, NT, 0, s>>>(
+            sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, log, log_nw);
+      else
+        k_render_screened<NT, true, true><<<(unsigned)ctas, NT, 0, s>>>(
+            sv, bv, cam, cfg, tile_begin, tile_stride, rgb, depth, trans, view, log, log_nw);
       return gsx_check_launch();
     }
   }
@@ -625,6 +646,8 @@ int gsx_validate_cfg(const gsx_render_cfg* cfg) {
   if (cfg->dt_min > cfg->dt_max) return GSX_ERR_ARG;
   if (cfg->mode != 0 && cfg->mode != 1) return GSX_ERR_ARG;
   if (!(cfg->dt > 0.0)) return GSX_ERR_ARG;
+  if (cfg->traversal < 0 || cfg->traversal > 2 || cfg->sums < 0 || cfg->sums > 1)
+    return GSX_ERR_ARG;
   return GSX_OK;
 }
 

@@ -789,12 +789,48 @@ struct Screen {
 #ifndef GSX_SCR_CH
 #define GSX_SCR_CH 16
 #endif
-struct WarpSmemS : WarpSmem {
+struct WarpSmemR : WarpSmem {  // screened forward, sums in registers
   uint32_t mask[LCAP];
+};
+struct WarpSmemS : WarpSmemR {  // screened forward, sums in shared memory
   float4 acc[GSX_SCR_CH][32];
 };
 
-__device__ inline void screen_list(const Screen& sc, WarpSmemS& sm, int count, unsigned lanes) {
+// Where a lane's per-sample sums live: its shared-memory column ...
+struct SmemSums {
+  float4* col;  // &acc[0][lane], stride 32
+  __device__ void zero(int ch) const {
+    for (int j = 0; j < ch; ++j) col[32 * j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ void add(int j, float dens, const float* c) const {
+    float4 a = col[32 * j];
+    a.x += dens;
+    a.y = fmaf(dens, c[0], a.y);
+    a.z = fmaf(dens, c[1], a.z);
+    a.w = fmaf(dens, c[2], a.w);
+    col[32 * j] = a;
+  }
+  __device__ float4 get(int j) const { return col[32 * j]; }
+};
+// ... or registers (a 64-register cap spills them to local memory)
+template <int CH>
+struct RegSums {
+  float sig[CH];
+  float W[CH][3];
+  __device__ void zero(int) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) sig[j] = W[j][0] = W[j][1] = W[j][2] = 0.f;
+  }
+  __device__ void add(int j, float dens, const float* c) {
+    sig[j] += dens;
+    W[j][0] = fmaf(dens, c[0], W[j][0]);
+    W[j][1] = fmaf(dens, c[1], W[j][1]);
+    W[j][2] = fmaf(dens, c[2], W[j][2]);
+  }
+  __device__ float4 get(int j) const { return make_float4(sig[j], W[j][0], W[j][1], W[j][2]); }
+};
+
+__device__ inline void screen_list(const Screen& sc, WarpSmemR& sm, int count, unsigned lanes) {
   const unsigned lane = threadIdx.x & 31;
   for (int b = 0; b < count; b += 32) {
     const int i = b + (int)lane;
@@ -843,9 +879,9 @@ __device__ inline void screen_list(const Screen& sc, WarpSmemS& sm, int count, u
 // 4-sample groups outside every lane's range skipped warp-uniformly); q <= 1
 // decides exactly, as in accumulate_used_at.  Returns the lane's smallest
 // accumulated q (2 if none).
-template <int CH>
+template <int CH, class Sums>
 __device__ inline float screened_samples(const CandUse& u, const float* c, float dtf,
-                                         float4* col) {
+                                         Sums& sums) {
   const CandSetup& cs = u.cs;
   const float nkl2 = -cs.kl2;
   float qmn = 2.f;
@@ -858,13 +894,7 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
       const float del = fmaf((float)j, dtf, cs.del0);
       const float q = fmaf(cs.A * del, del, cs.qmin);
       if (u.use && q <= 1.0f) {
-        const float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
-        float4 a = col[32 * j];
-        a.x += dens;
-        a.y = fmaf(dens, c[0], a.y);
-        a.z = fmaf(dens, c[1], a.z);
-        a.w = fmaf(dens, c[2], a.w);
-        col[32 * j] = a;
+        sums.add(j, ex2_approx(fmaf(nkl2, q, cs.lsig)), c);
         qmn = fminf(qmn, q);
       }
     }
@@ -873,7 +903,8 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
 }
 
 // Pass 1 over a screened list: entries no lane can use are skipped
-// warp-uniformly, and a lane sets up only the entries whose mask holds it.
+// warp-uniformly, and a lane sets up only the entries whose mask holds it;
+// the sums go to `sums` (SmemSums or RegSums).
 // (Taking the used entries two at a time, so their loads and radiance
 // evaluations interleave, measured slower: C3 37.4 vs 34.2 ms, C2 19.6 vs
 // 14.5 on one box -- the pair's second radiance is often wasted and the
@@ -882,13 +913,12 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
 // logged backward needs -- are also written, in list order, over the
 // already-consumed front of sm.mask (read back as int32); returns their
 // count.  sm.list stays whole for the exact emptiness test.
-template <int CH, bool COMPACT = false, class YT>
-__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemS& sm,
+template <int CH, bool COMPACT = false, class YT, class Sums>
+__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemR& sm,
                                           int count, bool want, int mc, const SegBase& base,
-                                          float dtf, YT Y, bool& inside) {
+                                          float dtf, YT Y, Sums& sums, bool& inside) {
   int kept = 0;
   const unsigned lane = threadIdx.x & 31;
-  float4* col = &sm.acc[0][lane];
   float qmn = 2.f;
   for (int i = 0; i < count; ++i) {
     const unsigned m = sm.mask[i];
@@ -902,7 +932,7 @@ __device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, 
     }
     float c[3] = {0.f, 0.f, 0.f};
     if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
-    qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, col));
+    qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
   }
   inside = inside || qmn <= 0.998f;
   if (COMPACT) __syncwarp();

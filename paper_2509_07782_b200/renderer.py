@@ -72,19 +72,67 @@ class MarchLog:
         return True
 
 
+# Forward kernel variants (all give the same pixels; gsx_render_cfg.sums and
+# the presence of a workspace select them): the silhouette-screened kernel
+# with per-sample sums in shared memory (16 warps / SM, no spills) or in
+# registers (32 warps / SM, spilled), and the unscreened packet-cone kernel.
+# Which one is fastest depends on the device's memory latency -- measured
+# across B200 boxes, the shared-memory kernel ranges from 8% faster to 14%
+# slower than the unscreened one -- so `autotune` times them on the
+# workload once and `render` uses the winner for that workload.
+VARIANTS = {"screened": (True, 0), "screened-regs": (True, 1), "plain": (False, 0)}
+_TUNED: dict = {}
+
+
+def _tune_key(scene, camera: Camera, cfg: RenderConfig, logged: bool, tile_stride: int):
+    return (scene.n, camera.width, camera.height, cfg.mode, bool(logged), int(tile_stride) > 1)
+
+
+def autotune(scene, camera: Camera, cfg: RenderConfig | None = None, *, log=None,
+             tile_begin: int = 0, tile_stride: int = 1, reps: int = 2) -> dict:
+    """Time every forward variant on this workload (device events, after one
+    warm-up each; synchronizes) and make the fastest the default of `render`
+    for workloads of this shape.  Returns {variant: ms, "best": name}."""
+    cfg = cfg or RenderConfig()
+    H, W = camera.height, camera.width
+    dev = scene.device
+    bufs = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev),
+            torch.empty((H, W), device=dev))
+    s = torch.cuda.current_stream()
+    out = {}
+    for name in VARIANTS:
+        def run():
+            render(scene, camera, cfg, tile_begin=tile_begin, tile_stride=tile_stride,
+                   rgb=bufs[0], depth=bufs[1], trans=bufs[2], log=log, variant=name)
+        run()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            run()
+        e1.record(s)
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
+    best = min(VARIANTS, key=lambda k: out[k])
+    _TUNED[_tune_key(scene, camera, cfg, log is not None, tile_stride)] = best
+    out["best"] = best
+    return out
+
+
 def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin: int = 0,
            tile_stride: int = 1, rgb=None, depth=None, trans=None, stats: bool = False,
-           log: MarchLog | None = None, stream=None, screen: bool = True, traversal: int = 0,
-           workspace=None):
+           log: MarchLog | None = None, stream=None, screen: bool | None = None,
+           traversal: int = 0, workspace=None, variant: str | None = None):
     """Render the 16x16 tiles tile_begin + k*tile_stride of `camera` into
     rgb [H,W,3], depth [H,W], trans [H,W] float32 CUDA tensors (allocated
     unless given).  Returns (rgb, depth, trans, stats_tensor_or_None).
     With `log` (training) the march is also recorded for render_backward.
-    `screen` enables the per-camera silhouette screen of the plain forward
-    (its table lives in `workspace`, default the scene's own render
-    workspace -- pass separate ones for concurrent renders of one scene);
-    `traversal` forces the warp traversal (0 auto, 1 cone, 2 per-lane).
-    Pixels do not depend on either."""
+    `variant` picks the forward kernel (VARIANTS; default: the one `autotune`
+    chose for this workload shape, else "screened"); `screen=False` is
+    variant "plain".  The screened kernels keep a per-camera silhouette table
+    in `workspace` (default the scene's own render workspace -- pass separate
+    ones for concurrent renders of one scene).  `traversal` forces the warp
+    traversal (0 auto, 1 cone, 2 per-lane).  Pixels do not depend on any of
+    these."""
     cfg = cfg or RenderConfig()
     L = _lib.lib()
     H, W = camera.height, camera.width
@@ -93,7 +141,11 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
     depth = _out((H, W), depth, dev)
     trans = _out((H, W), trans, dev)
     st = torch.zeros(10, dtype=torch.int64, device=dev) if stats else None
-    cam_c, cfg_c = camera.to_c(), cfg.to_c(traversal)
+    if variant is None:
+        variant = "plain" if screen is False else _TUNED.get(
+            _tune_key(scene, camera, cfg, log is not None, tile_stride), "screened")
+    screen, sums = VARIANTS[variant]
+    cam_c, cfg_c = camera.to_c(), cfg.to_c(traversal, sums)
     import ctypes
 
     if log is not None:

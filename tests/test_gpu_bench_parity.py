@@ -58,12 +58,16 @@ def _pixels(cam, stride, oy, ox):
 
 def _forward_subset(name, stride, oy, ox):
     G, rec, eps, scene, cam, cfg, cfg_kw = _setup(name)
-    rgb, depth, trans, _ = G.render(scene, cam, cfg)
-    rgb0, depth0, trans0, _ = G.render(scene, cam, cfg, screen=False)
+    tuned = G.autotune(scene, cam, cfg)
+    assert tuned["best"] in G.VARIANTS and all(tuned[k] > 0 for k in G.VARIANTS)
+    rgb, depth, trans, _ = G.render(scene, cam, cfg, variant="screened")
+    rgb0, depth0, trans0, _ = G.render(scene, cam, cfg, variant="plain")
+    rgb1 = G.render(scene, cam, cfg, variant="screened-regs")[0].cpu().numpy()
     rgb, depth, trans = rgb.cpu().numpy(), depth.cpu().numpy(), trans.cpu().numpy()
     # screened == unscreened up to fp32 contraction choices (bitwise on the
     # r06 build; a wrongly screened-out primitive would be orders above 2e-6)
     assert np.abs(rgb - rgb0.cpu().numpy()).max() <= 2e-6
+    assert np.abs(rgb - rgb1).max() <= 2e-6
     assert np.abs(trans - trans0.cpu().numpy()).max() <= 2e-6
     assert (np.abs(depth - depth0.cpu().numpy()) / np.maximum(1.0, depth)).max() <= 2e-6
     rays, py, px = _pixels(cam, stride, oy, ox)
