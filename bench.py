@@ -642,9 +642,51 @@ def main():
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         out["cpu_baseline"]["cpu_model"] = cpu_model()
         out["parity"] = parity_block(cb, cam_kw, *frame)
+        out["c1"] = c1_block(G, cb["cores"])
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c1_block(G, threads: int):
+    """BASELINE.json config 1 (10k Gaussians, 64x64, uniform + ESS -- the case
+    the reference's own CPU path runs): the GPU frame against the full-frame
+    oracle on all host threads, with both times and the parity of every pixel."""
+    import oracle as O
+    import torch
+
+    rec, eps, cam_kw, cfg_kw, desc = workload("c1")
+    cam = make_camera(G, cam_kw)
+    cfg = G.RenderConfig(**cfg_kw)
+    scene = G.Scene.from_records(rec, sigma_eps=eps)
+    G.reorder_by_morton(scene)
+    rgb, depth, trans, _ = G.render(scene, cam, cfg)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        G.render(scene, cam, cfg, rgb=rgb, depth=depth, trans=trans)
+    e1.record(s)
+    torch.cuda.synchronize()
+    gpu_ms = e0.elapsed_time(e1) / 10
+    t0 = time.time()
+    osc = O.OracleScene(rec, eps)
+    osc.reorder_by_morton()
+    build_s = time.time() - t0
+    rays = O.camera_rays(cam.center, cam.quat, cam.focal, cam.width, cam.height)
+    t0 = time.time()
+    R, T, D, _ = osc.march_rays(rays, O.OCfg.make(**cfg_kw), clip=True, threads=threads)
+    cpu_s = time.time() - t0
+    H, W = cam_kw["height"], cam_kw["width"]
+    return {"workload": desc, "gpu_ms": gpu_ms, "gpu_mrays": H * W / (gpu_ms * 1e-3) / 1e6,
+            "cpu_s": cpu_s, "cpu_mrays": H * W / cpu_s / 1e6, "cpu_cores": threads,
+            "cpu_kind": "port (oracle/, float64 C restatement of renderer.py)",
+            "cpu_scene_build_s": build_s,
+            "cpu_scene_build_note": "oracle Scene prep + its median-split BVH (the reference's "
+                                    "binned-SAH Python build is not available on the GPU host)",
+            "parity_full_frame": {
+                "max_abs_rgb": float(np.abs(rgb.cpu().numpy().reshape(-1, 3) - R).max()),
+                "max_abs_T": float(np.abs(trans.cpu().numpy().ravel() - T).max())}}
 
 
 def cpu_model() -> str:

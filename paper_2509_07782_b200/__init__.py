@@ -11,7 +11,7 @@ from .config import Camera, Ray, RenderConfig, RenderStats, quat_to_rotation, se
 from .geometry import (Aabb, GaussianShape, IsoLossConfig, aabb_of, ellipsoid_volume, iso_scale,
                        isotropic_loss, ratio_upper_bound, volume_ratio)
 from .densify import (DensifyConfig, GradAccumulator, criterion_new, criterion_old,
-                      neighbor_density, observe_scene)
+                      fd_position_gradient, neighbor_density, observe_scene)
 from .errors import (BufferOverflow, DegenerateCenter, EmptyIsosurface, EmptyScene, GsrayError,
                      ParseError, TraversalOverflow, ValidationError)
 from .renderer import (VARIANTS, MarchLog, autotune, clip_ray_to_scene, march_ray, march_rays,
@@ -49,5 +49,5 @@ __all__ = [
     "criterion_old", "eval_fields_batch", "load_ply_scene", "look_at_camera", "march_rays",
     "neighbor_density", "observe_scene", "orbit_cameras", "ply_records", "quat_to_rotation",
     "reference_rays", "render", "render_backward", "render_full", "sh_basis", "TraversalOverflow",
-    "VARIANTS", "autotune",
+    "VARIANTS", "autotune", "fd_position_gradient",
 ]

@@ -156,6 +156,42 @@ def neighbor_density(means, radius: float):
     return counts.cpu().numpy() if as_numpy else counts
 
 
+def fd_position_gradient(scene, camera, target, index: int, h: float | None = None,
+                         loss_cfg: LossConfig | None = None, render_cfg=None,
+                         iso_loss: float = 0.0):
+    """densify.py:156-187: central-difference gradient of the image loss
+    w.r.t. primitive `index`'s mean (storage index), by six device renders of
+    `scene.with_mean` copies (each a full K1-K5 rebuild, as the reference
+    rebuilds its Scene and BVH).  Renders default to uniform mode, the step
+    to 1e-4 x the scene diagonal.  The analytic gradient of the same loss is
+    `render_backward` (observe_scene uses it); this is the reference's
+    finite-difference API, e.g. to cross-check it."""
+    import numpy as np
+
+    from .config import RenderConfig
+    from .loss import image_loss
+    from .renderer import render
+
+    loss_cfg = loss_cfg or LossConfig()
+    render_cfg = render_cfg or RenderConfig(mode="uniform")
+    if h is None:
+        h = 1e-4 * float(np.linalg.norm(scene.bounds_hi - scene.bounds_lo))
+    mu = scene.params[index, 0:3].double().cpu().numpy()
+    tgt = torch.as_tensor(np.asarray(target, dtype=np.float32), device=scene.device)
+    grad = np.zeros(3)
+    for axis in range(3):
+        step = np.zeros(3)
+        step[axis] = h
+        losses, xs = [], []
+        for sgn in (1.0, -1.0):
+            m = (mu + sgn * step).astype(np.float32)  # the records are float32
+            img = render(scene.with_mean(index, m), camera, render_cfg)[0]
+            losses.append(image_loss(img, tgt, loss_cfg, iso_loss))
+            xs.append(float(m[axis]))
+        grad[axis] = (losses[0] - losses[1]) / (xs[0] - xs[1])
+    return grad
+
+
 def observe_scene(acc: GradAccumulator, scene, camera, target, indices=None,
                   loss_cfg: LossConfig | None = None, render_cfg=None):
     """Record one camera observation (densify.py:190-204): render, image loss,
