@@ -137,7 +137,7 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world:
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     ev[0].record(s)
-    scene.rebuild_async()
+    scene.rebuild_graphed()
     ev[1].record(s)
     render(scene, cam, cfg, rgb=tr.rgb, depth=tr.depth, trans=tr.trans, log=tr.log)
     ev[2].record(s)
@@ -435,13 +435,19 @@ def main():
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
-        scene._rebuild(validate=False)
+        scene.rebuild_graphed()
     e0.record(s)
     for _ in range(5):
-        scene._rebuild(validate=False)
+        scene.rebuild_graphed()
     e1.record(s)
     torch.cuda.synchronize()
     build_ms = e0.elapsed_time(e1) / 5
+    e0.record(s)
+    for _ in range(5):
+        scene.rebuild_async()
+    e1.record(s)
+    torch.cuda.synchronize()
+    build_eager_ms = e0.elapsed_time(e1) / 5
 
     # ---- algorithmic work counters (untimed stats pass)
     st = G.render(scene, cam, cfg, stats=True)[3]
@@ -625,7 +631,10 @@ def main():
         "gpu_launches": (2 if VARIANTS[tuned["best"]][0] else 1) * args.steps,
         "gpu_launches_note": "per frame: k_view_conics + k_render_screened (screened variants) "
         "or k_render_camera (plain)", "kernel": tuned,
-        "clocks": clk.summary(), "build_ms": build_ms, "setup_s": setup_s,
+        "clocks": clk.summary(), "build_ms": build_ms, "build_eager_ms": build_eager_ms,
+        "build_note": "K1-K5 rebuild (prepare, bounds, Morton, radix sort, LBVH + refit + "
+                      "4-wide collapse): CUDA-graph replay (build_ms) and eager launches",
+        "setup_s": setup_s,
         "counters_per_ray": {k: v / max(counters["rays"], 1) for k, v in counters.items()},
         "step_ms": step_ms,
     }

@@ -8,9 +8,13 @@
 // counter) merges its two children.  Leaves are single primitives in storage
 // order; each internal node stores both child boxes (fp32, outward-rounded
 // from the fp64 AABBs) so one 64-byte load tests both children.
+#include <cooperative_groups.h>
+
 #include "gsx_common.cuh"
 
 namespace {
+
+namespace cg = cooperative_groups;
 
 __device__ inline int delta(const uint64_t* __restrict__ codes, int64_t n, int64_t i, int64_t j) {
   if (j < 0 || j >= n) return -1;
@@ -202,12 +206,10 @@ __device__ inline float half_area(const float4& lo, const float4& hi) {
   return dx * dy + dy * dz + dz * dx;
 }
 
-__global__ void k_greedy_level(const float4* __restrict__ nodes, const QItem* __restrict__ qin,
-                               const uint32_t* __restrict__ nin_p, QItem* __restrict__ qout,
-                               uint32_t* nout_p, uint32_t* n4_p, float4* __restrict__ nodes4) {
-  const uint32_t nin = *nin_p;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += gridDim.x * blockDim.x) {
-    const QItem it = qin[i];
+__device__ inline void greedy_item(const float4* __restrict__ nodes, const QItem it,
+                                   QItem* __restrict__ qout, uint32_t* nout_p, uint32_t* n4_p,
+                                   float4* __restrict__ nodes4) {
+  {
     float4 lo[4], hi[4];
     int32_t ref[4];
     const float4* nd = nodes + 4 * (int64_t)it.bin;
@@ -274,11 +276,46 @@ __global__ void k_greedy_level(const float4* __restrict__ nodes, const QItem* __
   }
 }
 
+__global__ void k_greedy_level(const float4* __restrict__ nodes, const QItem* __restrict__ qin,
+                               const uint32_t* __restrict__ nin_p, QItem* __restrict__ qout,
+                               uint32_t* nout_p, uint32_t* n4_p, float4* __restrict__ nodes4) {
+  const uint32_t nin = *nin_p;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += gridDim.x * blockDim.x)
+    greedy_item(nodes, qin[i], qout, nout_p, n4_p, nodes4);
+}
+
+// The whole collapse in one cooperative launch: a grid-wide barrier per
+// frontier level and the termination decided on the device (the frontier
+// came out empty), so a rebuild has no host synchronization and can be
+// captured in a CUDA graph.  Frontier counters rotate over three slots:
+// level L reads c[L % 3], appends to c[(L + 1) % 3] and clears c[(L + 2) % 3],
+// which nobody touches during level L.
+__global__ void k_greedy_all(const float4* __restrict__ nodes, QItem* qa, QItem* qb,
+                             uint32_t* cnt, float4* __restrict__ nodes4) {
+  cg::grid_group grid = cg::this_grid();
+  uint32_t* c = cnt + 3;  // c[0..2] frontier sizes; cnt[2] = 4-wide slots used
+  for (int level = 0; level < 4 * 64; ++level) {
+    const QItem* qin = (level & 1) ? qb : qa;
+    QItem* qout = (level & 1) ? qa : qb;
+    uint32_t* cin = c + level % 3;
+    uint32_t* cout = c + (level + 1) % 3;
+    if (grid.thread_rank() == 0) c[(level + 2) % 3] = 0u;
+    const uint32_t nin = *cin;
+    for (uint32_t i = (uint32_t)grid.thread_rank(); i < nin; i += (uint32_t)grid.size())
+      greedy_item(nodes, qin[i], qout, cout, cnt + 2, nodes4);
+    grid.sync();
+    if (*(volatile uint32_t*)cout == 0u) break;  // the same value for every thread
+  }
+}
+
 __global__ void k_greedy_init(QItem* q, uint32_t* cnt) {
   q[0] = QItem{0, 0};
   cnt[0] = 1;  // frontier A size
   cnt[1] = 0;  // frontier B size
   cnt[2] = 1;  // BVH4 slots used (root = 0)
+  cnt[3] = 1;  // k_greedy_all's rotating frontier sizes
+  cnt[4] = 0;
+  cnt[5] = 0;
 }
 
 __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* children) {
@@ -303,8 +340,12 @@ extern "C" size_t gsx_bvh_workspace_bytes(int64_t n) {
          2 * gsx_align256(sizeof(QItem) * m) + 256;
 }
 
-// greedy collapse: level-synchronous frontier, host checks for completion every
-// GREEDY_BATCH levels (BVH4 depth is ~log4 n plus the LBVH's imbalance)
+// greedy collapse: level-synchronous frontier, one cooperative launch with
+// device-side termination (k_greedy_all); without GSX_GREEDY_COOP, one launch
+// per level and a host check for completion every GREEDY_BATCH levels
+#ifndef GSX_GREEDY_COOP
+#define GSX_GREEDY_COOP 1
+#endif
 static int greedy_collapse(const BvhView& bv, int64_t n, char* ws, cudaStream_t s) {
   constexpr int GREEDY_BATCH = 16;
   size_t seg = gsx_align256(sizeof(int32_t) * n);
@@ -316,6 +357,19 @@ static int greedy_collapse(const BvhView& bv, int64_t n, char* ws, cudaStream_t 
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#if GSX_GREEDY_COOP
+  {
+    int per_sm = 0;
+    CUDA_CHECK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_greedy_all, 256, 0));
+    const float4* nodes = bv.nodes;
+    float4* nodes4 = bv.nodes4;
+    void* args[] = {(void*)&nodes, (void*)&qa, (void*)&qb, (void*)&cnt, (void*)&nodes4};
+    CUDA_CHECK_RET(cudaLaunchCooperativeKernel((void*)k_greedy_all,
+                                               dim3((unsigned)(sms * (per_sm < 4 ? per_sm : 4))),
+                                               dim3(256), args, 0, s));
+    return gsx_check_launch();
+  }
+#endif
   const unsigned grid = (unsigned)(sms * 8);
   for (int level = 0;; ++level) {
     const int a = level & 1;

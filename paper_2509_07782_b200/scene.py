@@ -168,6 +168,33 @@ class Scene:
         check(L.gsx_bvh_build(ptr(self.arena), ptr(self.sorted_codes), ptr(self.morton_perm), n,
                               ptr(self.bvh_arena), ptr(self._bvh_ws), s), "bvh")
 
+    def rebuild_graphed(self):
+        """rebuild_async replayed from a CUDA graph (captured on first use, per
+        parameter buffer): the ~40 launches of K1-K5 (prepare, bounds,
+        Morton codes, 8 radix passes, Karras, refit, the cooperative 4-wide
+        collapse) go to the GPU as one graph launch.  Falls back to eager
+        launches if the capture fails."""
+        key = (self.params.data_ptr(), self.n)
+        g = getattr(self, "_rebuild_graph", None)
+        if g is None or getattr(self, "_rebuild_key", None) != key:
+            g = None
+            if not getattr(self, "_rebuild_no_graph", False):
+                try:
+                    self.rebuild_async()  # warm-up outside the capture
+                    torch.cuda.current_stream().synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        self.rebuild_async()
+                except Exception:  # (capture unsupported here: eager from now on)
+                    self._rebuild_no_graph = True
+                    g = None
+            self._rebuild_graph, self._rebuild_key = g, key
+        if g is None:
+            self.rebuild_async()
+            return
+        g.replay()
+        self.version = getattr(self, "version", 0) + 1
+
     # -- reference API -------------------------------------------------------
     def __len__(self) -> int:
         return self.n

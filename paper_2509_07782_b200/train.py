@@ -215,10 +215,12 @@ class Trainer:
 
     def __init__(self, scene, camera: Camera, cfg: RenderConfig | None = None,
                  loss_cfg: LossConfig = LossConfig(), iso_cfg: IsoLossConfig = IsoLossConfig(),
-                 lr=None, group=None, march_log: bool = True, densify=None):
+                 lr=None, group=None, march_log: bool = True, densify=None,
+                 graph_rebuild: bool = True):
         import torch.distributed as dist
 
         self.scene, self.camera = scene, camera
+        self.graph_rebuild = graph_rebuild  # K1-K5 replayed as one CUDA graph
         self.cfg = cfg or RenderConfig()
         self.loss_cfg, self.iso_cfg = loss_cfg, iso_cfg
         self.group = group
@@ -273,7 +275,7 @@ class Trainer:
         loss value (host sync) when want_loss, else None."""
         s = self.scene
         L = _lib.lib()
-        s.rebuild_async()
+        s.rebuild_graphed() if self.graph_rebuild else s.rebuild_async()
         render(s, self.camera, self.cfg, tile_begin=self.rank, tile_stride=self.world,
                rgb=self.rgb, depth=self.depth, trans=self.trans, log=self.log)
         gather_tiles([self.rgb, self.depth, self.trans], self.camera.width, self.camera.height,
