@@ -276,25 +276,33 @@ __device__ inline void greedy_item(const float4* __restrict__ nodes, const QItem
   }
 }
 
-__global__ void k_greedy_level(const float4* __restrict__ nodes, const QItem* __restrict__ qin,
-                               const uint32_t* __restrict__ nin_p, QItem* __restrict__ qout,
-                               uint32_t* nout_p, uint32_t* n4_p, float4* __restrict__ nodes4) {
-  const uint32_t nin = *nin_p;
+// Frontier counters rotate over three slots c[0..2] (= cnt[3..5]; cnt[2] is
+// the 4-wide slot count): level L reads c[L % 3], appends to c[(L + 1) % 3]
+// and clears c[(L + 2) % 3], which nobody touches during level L (it was level
+// L - 1's input).  No memsets and no host reads between levels.
+__global__ void k_greedy_level(const float4* __restrict__ nodes, QItem* qa, QItem* qb,
+                               uint32_t* cnt, float4* __restrict__ nodes4, int level) {
+  uint32_t* c = cnt + 3;
+  if (blockIdx.x == 0 && threadIdx.x == 0) c[(level + 2) % 3] = 0u;
+  const QItem* qin = (level & 1) ? qb : qa;
+  QItem* qout = (level & 1) ? qa : qb;
+  const uint32_t nin = c[level % 3];
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += gridDim.x * blockDim.x)
-    greedy_item(nodes, qin[i], qout, nout_p, n4_p, nodes4);
+    greedy_item(nodes, qin[i], qout, c + (level + 1) % 3, cnt + 2, nodes4);
 }
 
-// The whole collapse in one cooperative launch: a grid-wide barrier per
-// frontier level and the termination decided on the device (the frontier
-// came out empty), so a rebuild has no host synchronization and can be
-// captured in a CUDA graph.  Frontier counters rotate over three slots:
-// level L reads c[L % 3], appends to c[(L + 1) % 3] and clears c[(L + 2) % 3],
-// which nobody touches during level L.
+// The remaining levels from `first` on in one cooperative launch: a grid-wide
+// barrier per level and the termination decided on the device (a frontier
+// came out empty).  After GSX_GREEDY_LAUNCHED plain level launches the
+// frontiers left are the LBVH's deep, narrow tail, where a barrier costs less
+// than a launch; with no host synchronization a rebuild can be captured in a
+// CUDA graph.
 __global__ void k_greedy_all(const float4* __restrict__ nodes, QItem* qa, QItem* qb,
-                             uint32_t* cnt, float4* __restrict__ nodes4) {
+                             uint32_t* cnt, float4* __restrict__ nodes4, int first) {
   cg::grid_group grid = cg::this_grid();
-  uint32_t* c = cnt + 3;  // c[0..2] frontier sizes; cnt[2] = 4-wide slots used
-  for (int level = 0; level < 4 * 64; ++level) {
+  uint32_t* c = cnt + 3;
+  if (c[first % 3] == 0u) return;  // the plain launches finished the tree
+  for (int level = first; level < 4 * 64; ++level) {
     const QItem* qin = (level & 1) ? qb : qa;
     QItem* qout = (level & 1) ? qa : qb;
     uint32_t* cin = c + level % 3;
@@ -346,6 +354,9 @@ extern "C" size_t gsx_bvh_workspace_bytes(int64_t n) {
 #ifndef GSX_GREEDY_COOP
 #define GSX_GREEDY_COOP 1
 #endif
+#ifndef GSX_GREEDY_LAUNCHED  // plain level launches before the cooperative tail
+#define GSX_GREEDY_LAUNCHED 24
+#endif
 static int greedy_collapse(const BvhView& bv, int64_t n, char* ws, cudaStream_t s) {
   constexpr int GREEDY_BATCH = 16;
   size_t seg = gsx_align256(sizeof(int32_t) * n);
@@ -357,35 +368,31 @@ static int greedy_collapse(const BvhView& bv, int64_t n, char* ws, cudaStream_t 
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#if GSX_GREEDY_COOP
-  {
-    int per_sm = 0;
-    CUDA_CHECK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_greedy_all, 256, 0));
-    const float4* nodes = bv.nodes;
-    float4* nodes4 = bv.nodes4;
-    void* args[] = {(void*)&nodes, (void*)&qa, (void*)&qb, (void*)&cnt, (void*)&nodes4};
-    CUDA_CHECK_RET(cudaLaunchCooperativeKernel((void*)k_greedy_all,
-                                               dim3((unsigned)(sms * (per_sm < 4 ? per_sm : 4))),
-                                               dim3(256), args, 0, s));
-    return gsx_check_launch();
-  }
-#endif
   const unsigned grid = (unsigned)(sms * 8);
-  for (int level = 0;; ++level) {
-    const int a = level & 1;
-    QItem* qin = a ? qb : qa;
-    QItem* qout = a ? qa : qb;
-    CUDA_CHECK_RET(cudaMemsetAsync(cnt + (1 - a), 0, sizeof(uint32_t), s));
-    k_greedy_level<<<grid, 256, 0, s>>>(bv.nodes, qin, cnt + a, qout, cnt + (1 - a), cnt + 2,
-                                        bv.nodes4);
-    if ((level + 1) % GREEDY_BATCH == 0) {
+  const int launched = GSX_GREEDY_COOP ? GSX_GREEDY_LAUNCHED : 4 * 64;
+  for (int level = 0; level < launched; ++level) {
+    k_greedy_level<<<grid, 256, 0, s>>>(bv.nodes, qa, qb, cnt, bv.nodes4, level);
+#if !GSX_GREEDY_COOP
+    if ((level + 1) % GREEDY_BATCH == 0) {  // host-checked termination
       uint32_t h = 0;
-      CUDA_CHECK_RET(cudaMemcpyAsync(&h, cnt + (1 - a), sizeof h, cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK_RET(cudaMemcpyAsync(&h, cnt + 3 + (level + 1) % 3, sizeof h,
+                                     cudaMemcpyDeviceToHost, s));
       CUDA_CHECK_RET(cudaStreamSynchronize(s));
       if (h == 0) break;
-      if (level > 4 * 64) return GSX_ERR_STACK;  // cannot happen for a valid tree
     }
+#endif
   }
+#if GSX_GREEDY_COOP
+  int per_sm = 0;
+  CUDA_CHECK_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_greedy_all, 256, 0));
+  const float4* nodes = bv.nodes;
+  float4* nodes4 = bv.nodes4;
+  int first = launched;
+  void* args[] = {(void*)&nodes, (void*)&qa, (void*)&qb, (void*)&cnt, (void*)&nodes4,
+                  (void*)&first};
+  CUDA_CHECK_RET(cudaLaunchCooperativeKernel((void*)k_greedy_all, dim3((unsigned)(sms * per_sm)),
+                                             dim3(256), args, 0, s));
+#endif
   return gsx_check_launch();
 }
 
