@@ -47,7 +47,7 @@
 #define GSX_CHLEAF_ATTR __noinline__
 #endif
 #ifndef GSX_Y_SMEM
-#define GSX_Y_SMEM 1
+#define GSX_Y_SMEM 2  // SH basis: 1 shared memory, 2 recomputed per use (YDir), 0 registers
 #endif
 // camera-kernel traversal: 0 per-lane packet (warp_traverse), 1 packet cone
 // (warp_traverse_cone), 2 cone for the plain forward only
@@ -190,9 +190,9 @@ template <bool STATS, bool SAVE, bool CONE>
 __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayCtx& r, bool hit,
                               const gsx_render_cfg& cfg, RayAccum& acc, Counters<STATS>& cnt,
                               WarpSmem& sm, LogWriter& lw) {
+#if GSX_Y_SMEM == 1
   float Y[9];
   sh_basis_f(r.df, Y);
-#if GSX_Y_SMEM
   {
     const unsigned lane = threadIdx.x & 31;
 #pragma unroll
@@ -200,7 +200,11 @@ __device__ void march_forward(const SceneView& sv, const BvhView& bv, const RayC
     __syncwarp();
   }
   const YSmem Yv{&sm.ylane[0][threadIdx.x & 31]};
+#elif GSX_Y_SMEM == 2
+  const YDir Yv{r.df};
 #else
+  float Y[9];
+  sh_basis_f(r.df, Y);
   const float* Yv = Y;
 #endif
   const int ns = (int)cfg.n_s;
@@ -332,10 +336,14 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     int count = 0, kept = 0;
     for (;;) {
       warp_traverse_cone(bv, cst, sm, count, visits);
-      screen_list(sc, sm, count, lanes);
       bool inside = false;
-      kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sums,
-                                           inside);
+      if constexpr (SAVE) {
+        screen_list(sc, sm, count, lanes);
+        kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sums,
+                                             inside);
+      } else {
+        screen_accumulate<CH>(sc, sv, r, sm, count, lanes, wch, mc, base, dtf, Y, sums, inside);
+      }
       nonempty = nonempty || inside;
       // AABB emptiness without a clearly-inside sample: the exact test over
       // this chunk of the list (a superset of the boxes the segment meets)
@@ -347,7 +355,9 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
           }
       __syncwarp();
       if (cst.done) break;
-      if (save) log_list_chunk(lw, (const int32_t*)sm.mask, kept);
+      if constexpr (SAVE) {
+        if (save) log_list_chunk(lw, (const int32_t*)sm.mask, kept);
+      }
       __syncwarp();
       count = 0;
     }
@@ -390,7 +400,11 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
     k_render_screened(SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg,
                       int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
                       float* trans, const float4* view, void* log, long long log_nw) {
-  using WS = std::conditional_t<SMEM, WarpSmemS, WarpSmemR>;
+  constexpr int CH = GSX_SCR_CH;
+  // the training forward keeps the mask array (its used-entry compaction
+  // writes into it); the plain forward screens batch by batch in registers
+  using WS = std::conditional_t<SAVE, std::conditional_t<SMEM, WarpSmemS<CH>, WarpSmemR>,
+                                std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmem>>;
   __shared__ WS smem[NT / 32];
   WS& sw = smem[threadIdx.x >> 5];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
@@ -409,14 +423,18 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
   RayAccum acc;
   acc.init();
   const Screen sc{view, (float)((tile % tiles_x) * 16 + bx), (float)((tile / tiles_x) * 16 + by)};
+#if GSX_SCR_YSMEM == 1 && GSX_Y_SMEM == 1
   float Y[9];
   sh_basis_f(r.df, Y);
-#if GSX_SCR_YSMEM
 #pragma unroll
   for (int b = 0; b < 9; ++b) sw.ylane[b][lane] = Y[b];
   __syncwarp();
   const YSmem Yv{&sw.ylane[0][lane]};
+#elif GSX_SCR_YSMEM == 2 || GSX_Y_SMEM != 1
+  const YDir Yv{r.df};  // recomputed per radiance evaluation
 #else
+  float Y[9];
+  sh_basis_f(r.df, Y);
   const float* Yv = Y;  // (128 registers: the basis stays in registers)
 #endif
   const int ns = (int)cfg.n_s;

@@ -158,6 +158,27 @@ struct YSmem {
   __device__ float operator[](int b) const { return p[32 * b]; }
 };
 
+// ... or recomputed from the direction at each use (a handful of FMULs per
+// radiance evaluation instead of 9 live registers or 1.15 KB of shared
+// memory per warp); same values as sh_basis_f
+struct YDir {
+  const float* d;
+  __device__ float operator[](int b) const {
+    const float x = d[0], y = d[1], z = d[2];
+    switch (b) {
+      case 0: return 0.28209479177387814f;
+      case 1: return 0.4886025119029199f * y;
+      case 2: return 0.4886025119029199f * z;
+      case 3: return 0.4886025119029199f * x;
+      case 4: return 1.0925484305920792f * x * y;
+      case 5: return 1.0925484305920792f * y * z;
+      case 6: return 0.31539156525252005f * (3.0f * z * z - 1.0f);
+      case 7: return 1.0925484305920792f * x * z;
+      default: return 0.5462742152960396f * (x * x - y * y);
+    }
+  }
+};
+
 // unclamped radiance and lobe values (lobes may be NULL); app = GSX_APP_F4
 // float4 in the streaming layout, consumed one float4 at a time so the
 // coefficients never need 76 live registers.

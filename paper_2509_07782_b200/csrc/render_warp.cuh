@@ -82,7 +82,7 @@ struct WarpSmem {
   int32_t list[LCAP];
   int ovf;  // a traversal stack of this warp overflowed (reported as GSX_ERR_STACK)
   float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | dlo | dhi)
-#if GSX_Y_SMEM
+#if GSX_Y_SMEM == 1
   float ylane[9][32];  // per-lane SH basis (forward)
 #endif
 };
@@ -792,8 +792,13 @@ struct Screen {
 struct WarpSmemR : WarpSmem {  // screened forward, sums in registers
   uint32_t mask[LCAP];
 };
-struct WarpSmemS : WarpSmemR {  // screened forward, sums in shared memory
-  float4 acc[GSX_SCR_CH][32];
+template <int CH>
+struct WarpSmemS : WarpSmemR {  // screened training forward, sums in shared memory
+  float4 acc[CH][32];
+};
+template <int CH>
+struct WarpSmemA : WarpSmem {  // screened plain forward, sums in shared memory
+  float4 acc[CH][32];
 };
 
 // Where a lane's per-sample sums live: its shared-memory column ...
@@ -830,36 +835,35 @@ struct RegSums {
   __device__ float4 get(int j) const { return make_float4(sig[j], W[j][0], W[j][1], W[j][2]); }
 };
 
+// Silhouette mask of primitive p over the warp's 32 pixel centres.
+__device__ inline unsigned screen_entry(const Screen& sc, int64_t p) {
+  const float4 c0 = __ldg(sc.view + 2 * p);
+  if (!(c0.z > 0.f)) return FULL;
+  const float a11 = __ldg(sc.view + 2 * p + 1).x;
+  unsigned m = 0u;
+  float dx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dx[k] = (sc.x0 + (0.5f + (float)k)) - c0.x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float dy = (sc.y0 + (0.5f + (float)j)) - c0.y;
+    const float r1 = c0.w * dy, r2 = fmaf(a11 * dy, dy, -1.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      // Z-order lane of pixel (k, j): x bits at 0, 2, 4; y bits at 1, 3
+      const int l = (k & 1) | ((k & 2) << 1) | ((k & 4) << 2) | ((j & 1) << 1) | ((j & 2) << 2);
+      const float q = fmaf(dx[k], fmaf(c0.z, dx[k], r1), r2);
+      m |= q <= 0.f ? (1u << l) : 0u;
+    }
+  }
+  return m;
+}
+
 __device__ inline void screen_list(const Screen& sc, WarpSmemR& sm, int count, unsigned lanes) {
   const unsigned lane = threadIdx.x & 31;
   for (int b = 0; b < count; b += 32) {
     const int i = b + (int)lane;
-    unsigned m = 0u;
-    if (i < count) {
-      const int64_t p = sm.list[i];
-      const float4 c0 = __ldg(sc.view + 2 * p);
-      if (c0.z > 0.f) {
-        const float a11 = __ldg(sc.view + 2 * p + 1).x;
-        float dx[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dx[k] = (sc.x0 + (0.5f + (float)k)) - c0.x;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float dy = (sc.y0 + (0.5f + (float)j)) - c0.y;
-          const float r1 = c0.w * dy, r2 = fmaf(a11 * dy, dy, -1.f);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            // Z-order lane of pixel (k, j): x bits at 0, 2, 4; y bits at 1, 3
-            const int l = (k & 1) | ((k & 2) << 1) | ((k & 4) << 2) | ((j & 1) << 1) | ((j & 2) << 2);
-            const float q = fmaf(dx[k], fmaf(c0.z, dx[k], r1), r2);
-            m |= q <= 0.f ? (1u << l) : 0u;
-          }
-        }
-      } else {
-        m = FULL;
-      }
-      sm.mask[i] = m & lanes;
-    }
+    if (i < count) sm.mask[i] = screen_entry(sc, sm.list[i]) & lanes;
   }
   __syncwarp();
 }
@@ -937,6 +941,40 @@ __device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, 
   inside = inside || qmn <= 0.998f;
   if (COMPACT) __syncwarp();
   return COMPACT ? kept : count;
+}
+
+// Screen + pass 1 in batches of 32 list entries without a mask array: lane
+// e screens entry b + e and keeps its mask in a register; the batch's
+// screened-in entries are then processed in list order with the mask and
+// the primitive broadcast by shuffles.  Same entries, same order, same
+// arithmetic as screen_list + accumulate_screened, 1 KB less shared memory
+// per warp (more L1 for the register-sum variant, more warps for the
+// shared-memory one).
+template <int CH, class YT, class Sums>
+__device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, const RayCtx& r,
+                                         const WarpSmem& sm, int count, unsigned lanes,
+                                         bool want, int mc, const SegBase& base, float dtf, YT Y,
+                                         Sums& sums, bool& inside) {
+  const unsigned lane = threadIdx.x & 31;
+  float qmn = 2.f;
+  for (int b = 0; b < count; b += 32) {
+    const int i = b + (int)lane;
+    const int32_t pl = i < count ? sm.list[i] : 0;
+    const unsigned ml = i < count ? screen_entry(sc, pl) & lanes : 0u;
+    unsigned todo = __ballot_sync(FULL, ml != 0u);
+    while (todo) {
+      const int e = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const unsigned m = __shfl_sync(FULL, ml, e);
+      const int64_t p = __shfl_sync(FULL, pl, e);
+      const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
+      if (!__any_sync(FULL, u.use)) continue;
+      float c[3] = {0.f, 0.f, 0.f};
+      if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
+      qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
+    }
+  }
+  inside = inside || qmn <= 0.998f;
 }
 
 // Exact AABB-emptiness of the lane's segment (reference semantics) after the
