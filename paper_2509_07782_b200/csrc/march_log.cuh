@@ -17,11 +17,13 @@
 // lanes waiting in most iterations) are stored, in slot order
 // slot = popc(act & lanes below):
 //   kind 0 (full):  double tb[nact], double dt[nact], int32 mc[nact],
-//                   float4 smp[mmax][nact] (sigma, W0, W1, W2), int32 list[count]
-//                   (each array 16-byte aligned, see LogLayout)
-//   kind 1 (list):  int32 list[count]   (a leading chunk of a candidate stream
-//                   longer than the shared list; the kind-0 record that
-//                   follows holds the rest and the sample sums)
+//                   float4 smp[mmax][nact] (sigma, W0, W1, W2), int32 list[count],
+//                   uint32 umask[count] (each array 16-byte aligned, see LogLayout)
+//   kind 1 (list):  int32 list[count], uint32 umask[count]  (a leading chunk of
+//                   a candidate stream longer than the shared list; the kind-0
+//                   record that follows holds the rest and the sample sums)
+// umask[i] = the lanes (bit = lane) whose setup of list[i] succeeded in the
+// forward: exactly the (lane, primitive) pairs the backward's pass 2 visits.
 // A warp whose records did not fit (bump pointer past capacity) is marked
 // complete = 0 and the backward recomputes it with the replay kernel.
 #pragma once
@@ -35,7 +37,8 @@ struct LogHeader {
   unsigned int overflow;
   unsigned int nwarps;
   unsigned long long need;  // bytes every record would need (incl. those that did not fit)
-  unsigned int pad[24];
+  unsigned long long entries, pairs;  // logged list entries, sum of their use-mask popcounts
+  unsigned int pad[20];
 };
 static_assert(sizeof(LogHeader) == 128, "LogHeader is one 128-byte line");
 
@@ -54,15 +57,21 @@ __host__ __device__ inline long long log_round16(long long x) { return (x + 15) 
 
 // byte offsets inside a kind-0 body for nact stored lanes
 struct LogLayout {
-  long long dt, mc, smp, list, bytes;
+  long long dt, mc, smp, list, umask, bytes;
   __host__ __device__ LogLayout(int nact, int mmax, int count) {
     dt = 8LL * nact;
     mc = 16LL * nact;
     smp = log_round16(20LL * nact);
     list = smp + 16LL * nact * mmax;
-    bytes = 128 + log_round128(list + 4LL * count);
+    umask = list + log_round16(4LL * count);
+    bytes = 128 + log_round128(umask + 4LL * count);
   }
 };
+// offset of umask in a kind-1 body and the record's bytes
+__host__ __device__ inline long long log_chunk_umask(int count) { return log_round16(4LL * count); }
+__host__ __device__ inline long long log_chunk_bytes(int count) {
+  return 128 + log_round128(log_chunk_umask(count) + 4LL * count);
+}
 __host__ __device__ inline long long log_table_bytes(long long nw) {
   return log_round128(128 + 8 * nw) + log_round128(4 * nw);
 }
@@ -85,6 +94,7 @@ struct LogWriter {
   long long first, prev;
   long long wid;
   long long need;  // bytes this warp's records need, logged or not
+  unsigned entries, pairs;  // this lane's share of the logged entries / pairs
   bool on;
 };
 
@@ -95,6 +105,7 @@ __device__ inline LogWriter log_writer(void* base, long long wid) {
   w.prev = -1;
   w.wid = wid;
   w.need = 0;
+  w.entries = w.pairs = 0u;
   w.on = base != nullptr;
   return w;
 }
@@ -140,8 +151,15 @@ __device__ inline void log_header(const LogWriter& w, long long off, int count, 
 
 // The log streams through L2 once each way: evict-first stores/loads keep
 // the scene and BVH resident.
-__device__ inline void log_list(int32_t* dst, const int32_t* list, int count) {
-  for (int i = threadIdx.x & 31; i < count; i += 32) __stcs(dst + i, list[i]);
+__device__ inline void log_list(LogWriter& w, int32_t* dst, const int32_t* list, uint32_t* mdst,
+                                const uint32_t* umask, int count) {
+  for (int i = threadIdx.x & 31; i < count; i += 32) {
+    const uint32_t m = umask[i];
+    __stcs(dst + i, list[i]);
+    __stcs(mdst + i, m);
+    w.entries += 1u;
+    w.pairs += (unsigned)__popc(m);
+  }
 }
 
 // The record writers run once per warp iteration inside the march loop; kept
@@ -157,21 +175,23 @@ __device__ inline void log_list(int32_t* dst, const int32_t* list, int count) {
 #endif
 
 // kind 1: a full shared-list chunk of a long candidate stream
-__device__ GSX_LOG_ATTR void log_list_chunk(LogWriter& w, const int32_t* list, int count) {
+__device__ GSX_LOG_ATTR void log_list_chunk(LogWriter& w, const int32_t* list,
+                                            const uint32_t* umask, int count) {
   if (!w.base) return;
-  const long long off = log_alloc(w, 128 + log_round128(4LL * count));
+  const long long off = log_alloc(w, log_chunk_bytes(count));
   if (off < 0) return;
   log_header(w, off, count, 1, 0, 0u);
-  log_list((int32_t*)(w.base + off + 128), list, count);
+  char* body = w.base + off + 128;
+  log_list(w, (int32_t*)body, list, (uint32_t*)(body + log_chunk_umask(count)), umask, count);
 }
 
 // kind 0 without the sample sums: allocates the record, writes its header,
 // the lane block (tb, dt, mc) and the list; returns the lane's first
 // sample-sum slot (nullptr for lanes without samples or on overflow) and the
 // warp-uniform stride nact / row count mmax of the sample-sum array.
-__device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list, int count,
-                                              double tb, double dt, int mc, int& nact_out,
-                                              int& mmax_out) {
+__device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list,
+                                              const uint32_t* umask, int count, double tb,
+                                              double dt, int mc, int& nact_out, int& mmax_out) {
   const int lane = threadIdx.x & 31;
   const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
   const int nact = __popc(act);
@@ -184,7 +204,7 @@ __device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list,
   mmax_out = mmax;
   log_header(w, off, count, 0, mmax, act);
   char* body = w.base + off + 128;
-  log_list((int32_t*)(body + L.list), list, count);
+  log_list(w, (int32_t*)(body + L.list), list, (uint32_t*)(body + L.umask), umask, count);
   if (mc <= 0) return nullptr;
   const int slot = __popc(act & ((1u << lane) - 1u));
   __stcs((double*)body + slot, tb);
@@ -194,12 +214,12 @@ __device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list,
 }
 
 // kind 0: the active lanes' block, their per-sample sums, the last list chunk
-__device__ inline void log_full(LogWriter& w, const int32_t* list, int count, double tb,
-                                double dt, int mc, const float (&sig)[16],
-                                const float (&W)[16][3]) {
+__device__ inline void log_full(LogWriter& w, const int32_t* list, const uint32_t* umask,
+                                int count, double tb, double dt, int mc,
+                                const float (&sig)[16], const float (&W)[16][3]) {
   if (!w.base) return;
   int nact, mmax;
-  float4* smp = log_full_head(w, list, count, tb, dt, mc, nact, mmax);
+  float4* smp = log_full_head(w, list, umask, count, tb, dt, mc, nact, mmax);
   if (smp) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -213,11 +233,11 @@ __device__ inline void log_full(LogWriter& w, const int32_t* list, int count, do
 
 // kind 0 from the screened forward's sums (sums.get(j) = (sigma_j, W_j))
 template <class Sums>
-__device__ inline void log_full_sums(LogWriter& w, const int32_t* list, int count, double tb,
-                                     double dt, int mc, const Sums& sums) {
+__device__ inline void log_full_sums(LogWriter& w, const int32_t* list, const uint32_t* umask,
+                                     int count, double tb, double dt, int mc, const Sums& sums) {
   if (!w.base) return;
   int nact, mmax;
-  float4* smp = log_full_head(w, list, count, tb, dt, mc, nact, mmax);
+  float4* smp = log_full_head(w, list, umask, count, tb, dt, mc, nact, mmax);
   if (smp) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -228,7 +248,17 @@ __device__ inline void log_full_sums(LogWriter& w, const int32_t* list, int coun
 
 // end of the warp: publish its chain head and whether it is complete
 __device__ inline void log_finish(const LogWriter& w, long long nw) {
-  if (!w.base || (threadIdx.x & 31) != 0) return;
+  if (!w.base) return;
+  unsigned long long e = w.entries, pr = w.pairs;
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    pr += __shfl_xor_sync(0xffffffffu, pr, o);
+  }
+  if ((threadIdx.x & 31) != 0) return;
+  if (e) {
+    atomicAdd(&((LogHeader*)w.base)->entries, e);
+    atomicAdd(&((LogHeader*)w.base)->pairs, pr);
+  }
   log_first(w.base)[w.wid] = w.on ? w.first : -1;
   log_complete(w.base, nw)[w.wid] = w.on ? 1u : 0u;
   atomicAdd(&((LogHeader*)w.base)->need, (unsigned long long)w.need);

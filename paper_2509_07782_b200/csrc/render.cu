@@ -90,6 +90,10 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
   constexpr int CH = SAVE ? 16 : GSX_FWD_CH;
   const int nchunks = (ns + CH - 1) / CH;
   uint32_t visits = 0;
+  // the training forward's smem is a WarpSmemR: its mask array takes the
+  // kept entries' use masks (k_render_camera)
+  uint32_t* umask = nullptr;
+  if constexpr (SAVE) umask = static_cast<WarpSmemR&>(sm).mask;
   for (int ch = 0; ch < nchunks; ++ch) {
     int mc = want ? seg.m - ch * CH : 0;
     mc = mc < 0 ? 0 : (mc > CH ? CH : mc);
@@ -139,15 +143,16 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       PH_END(1, ph_t)
       PH_BEGIN(ph_p)
       // the logged forward records only the entries some lane used
-      count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact);
+      count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, umask,
+                                    exact);
       PH_END(2, ph_p)
       if (CONE ? cst.done : st.done) break;
-      if (save) log_list_chunk(lw, sm.list, count);
+      if (save) log_list_chunk(lw, sm.list, umask, count);
       __syncwarp();
       count = 0;
     }
     if constexpr (SAVE) {
-      if (save) log_full(lw, sm.list, count, tb, seg.dt, mc, sig, W);
+      if (save) log_full(lw, sm.list, umask, count, tb, seg.dt, mc, sig, W);
     }
     if (STATS) {
 #pragma unroll
@@ -284,7 +289,8 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
     SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
     int64_t tile_stride, float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
     long long log_nw) {
-  __shared__ WarpSmem smem[NT / 32];
+  using WS = std::conditional_t<SAVE, WarpSmemR, WarpSmem>;
+  __shared__ WS smem[NT / 32];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   render_warp_block<STATS, SAVE, CONE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
                                  trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
@@ -356,13 +362,13 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       __syncwarp();
       if (cst.done) break;
       if constexpr (SAVE) {
-        if (save) log_list_chunk(lw, (const int32_t*)sm.mask, kept);
+        if (save) log_list_chunk(lw, (const int32_t*)sm.mask, sm.umask, kept);
       }
       __syncwarp();
       count = 0;
     }
     if constexpr (SAVE) {
-      if (save) log_full_sums(lw, (const int32_t*)sm.mask, kept, tb, seg.dt, mc, sums);
+      if (save) log_full_sums(lw, (const int32_t*)sm.mask, sm.umask, kept, tb, seg.dt, mc, sums);
     }
     // front-to-back compositing (renderer.py:230-239)
 #pragma unroll
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
   constexpr int CH = GSX_SCR_CH;
   // the training forward keeps the mask array (its used-entry compaction
   // writes into it); the plain forward screens batch by batch in registers
-  using WS = std::conditional_t<SAVE, std::conditional_t<SMEM, WarpSmemS<CH>, WarpSmemR>,
+  using WS = std::conditional_t<SAVE, std::conditional_t<SMEM, WarpSmemS<CH>, WarpSmemL>,
                                 std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmem>>;
   __shared__ WS smem[NT / 32];
   WS& sw = smem[threadIdx.x >> 5];
@@ -741,6 +747,8 @@ __global__ void k_log_init(LogHeader* h, unsigned long long cap, unsigned nw, lo
   h->overflow = 0;
   h->nwarps = nw;
   h->need = (unsigned long long)table;
+  h->entries = 0;
+  h->pairs = 0;
 }
 
 extern "C" int64_t gsx_march_log_min_bytes(const gsx_camera* cam, int64_t tile_begin,

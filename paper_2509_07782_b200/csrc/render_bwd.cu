@@ -357,7 +357,7 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
         if (want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
       };
       for (;;) {
-        accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact);
+        accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, nullptr, exact);
         if (st.done) break;
         __syncwarp();
         count = 0;
@@ -402,6 +402,262 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
   }
   emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt, sm.ovf);
   return nonempty;
+}
+
+// ---------------------------------------------------------------------------
+// Logged pass 2 over (lane, primitive) pairs.  The forward logged, per kept
+// list entry, the lanes whose setup of it succeeded (march_log.cuh umask):
+// about a third of the warp per entry.  Walking the entries with all 32
+// lanes in lockstep (grad_candidate) idles the rest through the setup,
+// radiance and moment work and reduces 86 mostly-zero columns per entry.
+// Here a list's pairs are enumerated in entry order and taken 32 at a time:
+// lane k works pair k with its ray's data (direction, segment base, sample
+// adjoints) read from the warp's lane table, and the 86 per-pair values are
+// summed per entry over the entry's run of lanes (a segmented column sum
+// through shared memory, one row per lane) in three passes of <= 32 rows:
+//   P1: geometry moments (10) + SH values 0-21      -> batch / atomics
+//   P2: lobes 0-3 (7 rows each)                     -> batch (axes) / atomics
+//   P3: SH values 22-26 + lobes 4-6                 -> atomics / batch
+// An entry split by a 32-pair boundary contributes two batch rows; every
+// finished value is linear in them, so the atomics add up the same.
+// ---------------------------------------------------------------------------
+constexpr int PR_ROW = 36;  // a row per lane, 32 pair columns (16-byte rows: float4 reads conflict-free)
+constexpr int PR_FLOATS = 32 * PR_ROW;
+constexpr int LT_ROWS = 14;  // lane table: df[3], base.hi[3], base.lo[3], dtf, mc, gC[3]
+constexpr int WH_FLOATS = 2 * 16 * 32;  // wos[16][32], hh[16][32]
+constexpr int PAIR_RUNS = 32;  // entries (runs) per pair batch = batch rows of the finish
+constexpr int PAIR_WARP_FLOATS = PR_FLOATS + WH_FLOATS + LT_ROWS * 32 + PAIR_RUNS * BAT_ROW;
+
+struct PairBufs {
+  float* pr;  // PR_FLOATS
+  float* wh;  // WH_FLOATS
+  float* lt;  // LT_ROWS x 32
+};
+
+// position of the n-th (0-based) set bit of m
+__device__ inline int nth_bit(unsigned m, int n) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w; w >>= 1) {
+    const unsigned lo = m & ((1u << w) - 1u);
+    const int c = __popc(lo);
+    if (n >= c) {
+      n -= c;
+      m >>= w;
+      pos += w;
+    } else {
+      m = lo;
+    }
+  }
+  return pos;
+}
+
+// Sum rows [0, nrows) of the pass buffer over each run of `ends` (bit k set:
+// pair k is the last of its entry in this batch) and hand (row, sum, entry's
+// primitive, run index) to emit.  Lane = row: one pass over the 32 columns
+// (float4 loads), the running sum restarted after each run end (a
+// warp-uniform select) and stored over the run's last column; then one emit
+// per (row, run).
+template <class Emit>
+__device__ inline void pair_reduce(const PairBufs& pb, unsigned ends, int pe, int nrows,
+                                   Emit&& emit) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  float* rp = pb.pr + lane * PR_ROW;
+  if (lane < nrows) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k4 = 0; k4 < 8; ++k4) {
+      const float4 v = *(const float4*)(rp + 4 * k4);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int k = 4 * k4 + c;
+        acc = (k > 0 && ((ends >> (k - 1)) & 1u)) ? vv[c] : acc + vv[c];
+        if ((ends >> k) & 1u) rp[k] = acc;
+      }
+    }
+  }
+  __syncwarp();
+  int run = 0;
+  while (ends) {
+    const int k1 = __ffs(ends) - 1;
+    ends &= ends - 1;
+    const int pseg = __shfl_sync(FULL, pe, k1);
+    if (lane < nrows) emit(lane, rp[k1], (int64_t)pseg, run);
+    ++run;
+  }
+  __syncwarp();
+}
+
+// Pass 2 over one logged list (entries + use masks) of the current record.
+// (Routing the entries most lanes use through the all-lanes path instead
+// (grad_candidate) measured slower: C2 17.0 vs 14.3 ms.)
+__device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb,
+                          const int32_t* __restrict__ list, const uint32_t* __restrict__ umask,
+                          int count, float* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 < count; i0 += 32) {
+    const bool have = i0 + lane < count;
+    const int ent = have ? __ldcs(list + i0 + lane) : 0;
+    const unsigned em = have ? __ldcs(umask + i0 + lane) : 0u;
+    int incl = __popc(em);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    // batches of <= 32 pairs from <= PAIR_RUNS entries
+    for (int b0 = 0; b0 < total;) {
+      const int g = b0 + lane;
+      // entry of pair g: the number of entries whose inclusive count is <= g
+      int e = 0;
+#pragma unroll
+      for (int st = 16; st; st >>= 1)
+        if (__shfl_sync(FULL, incl, e + st - 1) <= g) e += st;
+      const int e0b = __shfl_sync(FULL, e, 0);
+      const int bend = min(min(b0 + 32, total),
+                           e0b + PAIR_RUNS < 32 ? __shfl_sync(FULL, incl, e0b + PAIR_RUNS - 1)
+                                                : total);
+      const bool valid = g < bend;
+      const int pe = __shfl_sync(FULL, ent, e);
+      const unsigned me = __shfl_sync(FULL, em, e);
+      const int ex = __shfl_sync(FULL, incl, e) - __popc(me);
+      const int src = valid ? nth_bit(me, g - ex) : 0;
+      const int last = bend - b0 - 1;
+      const int en = __shfl_down_sync(FULL, e, 1);
+      const unsigned ends = __ballot_sync(FULL, valid && (lane == last || en != e));
+      const int nrun = __popc(ends);
+      b0 = bend;
+      if (gb.n + nrun > PAIR_RUNS) grad_batch_flush(sv, gb, grad);
+
+      // ---- the pair: setup, radiance, moments (renderer.py:207-240 adjoint)
+      const float* lt = pb.lt + src;
+      RayCtx rr;
+      rr.df[0] = lt[0];
+      rr.df[1] = lt[32];
+      rr.df[2] = lt[64];
+      SegBase base;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        base.hi[k] = lt[(3 + k) * 32];
+        base.lo[k] = lt[(6 + k) * 32];
+      }
+      const float dtf = lt[9 * 32];
+      const int mc = __float_as_int(lt[10 * 32]);
+      const float gC[3] = {lt[11 * 32], lt[12 * 32], lt[13 * 32]};
+      const int64_t p = pe;
+      CandSetup cs;
+      int jlo = 0, jhi = -1;
+      const bool use = valid && cand_setup_at(sv.geo + 4 * p, rr, base, cs) &&
+                       sample_range(cs, dtf, mc, jlo, jhi);
+      const YDir Y{rr.df};
+      float pre[3] = {0.f, 0.f, 0.f};
+      if (use) eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, rr.df, pre, nullptr);
+      const float gcl = gC[0] * fmaxf(pre[0], 0.f) + gC[1] * fmaxf(pre[1], 0.f) +
+                        gC[2] * fmaxf(pre[2], 0.f);
+      float m0 = 0.f, m1 = 0.f, m2 = 0.f, e0 = 0.f;
+      if (use) {
+        const float nkl2 = -cs.kl2;
+        const float* wo = pb.wh + src;
+        const float* hp = pb.wh + 512 + src;
+        for (int j = jlo; j <= jhi; ++j) {
+          const float del = fmaf((float)j, dtf, cs.del0);
+          const float q = fmaf(cs.A * del, del, cs.qmin);
+          if (q <= 1.0f) {
+            const float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
+            const float w = wo[32 * j];
+            const float G = fmaf(w, gcl, hp[32 * j]) * dens;
+            const float t = (float)j * dtf;
+            m0 += G;
+            m1 = fmaf(G, t, m1);
+            m2 = fmaf(G * t, t, m2);
+            e0 = fmaf(w, dens, e0);
+          }
+        }
+      }
+      float gpc[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gpc[c] = (use && pre[c] > 0.f) ? gC[c] * e0 : 0.f;
+      float* col = pb.pr + lane;
+      float* const gb_bat = gb.bat;
+      const int nb = gb.n;
+
+      // ---- P1: geometry moments + SH 0-21
+      {
+        const float4 g0 = __ldg(sv.geo + 4 * p);
+        const float v0[3] = {(base.hi[0] - g0.x) + base.lo[0], (base.hi[1] - g0.y) + base.lo[1],
+                             (base.hi[2] - g0.z) + base.lo[2]};
+        const float* d = rr.df;
+        col[0] = m0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) col[(1 + a) * PR_ROW] = fmaf(v0[a], m0, d[a] * m1);
+        const int ia[6] = {0, 1, 2, 0, 0, 1}, ib[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const float va = v0[ia[q]], vb = v0[ib[q]], da = d[ia[q]], db = d[ib[q]];
+          col[(4 + q) * PR_ROW] = fmaf(va * vb, m0, fmaf(fmaf(va, db, da * vb), m1, da * db * m2));
+        }
+#pragma unroll
+        for (int idx = 0; idx < 22; ++idx) col[(10 + idx) * PR_ROW] = Y[idx / 3] * gpc[idx % 3];
+      }
+      pair_reduce(pb, ends, pe, 32, [&](int row, float sum, int64_t ps, int run) {
+        float* brow = gb_bat + (nb + run) * BAT_ROW;
+        if (row < 10) {
+          brow[row] = sum;
+          if (row == 0) brow[31] = __int_as_float((int)ps);
+        } else if (sum != 0.f) {
+          atomicAdd(grad + (int64_t)GSX_NREC * ps + 11 + (row - 10), sum);
+        }
+      });
+
+      // ---- P2 / P3: spherical-Gaussian lobes (+ the last 5 SH values in P3)
+      const float4* ap = sv.app + GSX_APP_F4 * p;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int lb0 = pass == 0 ? 0 : 4, nl = pass == 0 ? 4 : 3, r0 = pass == 0 ? 0 : 5;
+        if (pass == 1) {
+#pragma unroll
+          for (int idx = 22; idx < 27; ++idx) col[(idx - 22) * PR_ROW] = Y[idx / 3] * gpc[idx % 3];
+        }
+#pragma unroll 1
+        for (int l = lb0; l < lb0 + nl; ++l) {
+          float* c = col + (r0 + 7 * (l - lb0)) * PR_ROW;
+          if (use) {
+            const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
+            const float cs2 = fmaf(ax.x, rr.df[0], fmaf(ax.y, rr.df[1], ax.z * rr.df[2]));
+            const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
+            const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
+            const float f = lb * ax.w * ga;
+            c[0] = f * rr.df[0];
+            c[PR_ROW] = f * rr.df[1];
+            c[2 * PR_ROW] = f * rr.df[2];
+            c[3 * PR_ROW] = lb * (cs2 - 1.f) * ga;
+            c[4 * PR_ROW] = lb * gpc[0];
+            c[5 * PR_ROW] = lb * gpc[1];
+            c[6 * PR_ROW] = lb * gpc[2];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 7; ++k) c[k * PR_ROW] = 0.f;
+          }
+        }
+        pair_reduce(pb, ends, pe, r0 + 7 * nl, [&](int row, float sum, int64_t ps, int run) {
+          if (row < r0) {
+            if (sum != 0.f) atomicAdd(grad + (int64_t)GSX_NREC * ps + 11 + 22 + row, sum);
+            return;
+          }
+          const int l = lb0 + (row - r0) / 7, k = (row - r0) % 7;
+          if (k < 3)
+            gb_bat[(nb + run) * BAT_ROW + 10 + 3 * l + k] = sum;
+          else if (sum != 0.f)
+            atomicAdd(grad + (int64_t)GSX_NREC * ps + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)),
+                      sum);
+        });
+      }
+      gb.n = nb + nrun;
+    }
+  }
 }
 
 // Per-pixel adjoint inputs from the saved frame outputs.
@@ -500,35 +756,56 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
 #ifndef GSX_BWD_LDGRP
 #define GSX_BWD_LDGRP 1
 #endif
-#ifndef GSX_BWDL_THREADS
-#define GSX_BWDL_THREADS 128
+// Two pass-2 strategies over the same records (one launch each; the log's
+// pair statistics pick one on the device, the other kernel's warps return at
+// once -- no host synchronization):
+//   PAIRS   (64-thread CTAs x 7): the pair batches above;
+//   entries (128-thread CTAs x 4): all 32 lanes per list entry
+//           (grad_candidate), the better choice when most lanes use most
+//           entries.  C2 (14.1 lanes per entry) 12.6 vs 13.4 ms; C4 (7.7)
+//           26.5 vs 17.3 ms.
+#ifndef GSX_BWDL_PAIR_MAX  // mean lanes per entry (x 1/16) below which PAIRS runs
+#define GSX_BWDL_PAIR_MAX 192
 #endif
-#ifndef GSX_BWDL_MINB
-#define GSX_BWDL_MINB 4
-#endif
-constexpr int BWDL_THREADS = GSX_BWDL_THREADS;
-constexpr int BWDL_PER_TILE = 256 / BWDL_THREADS;
+template <bool PAIRS>
+struct BwdlShape;
+template <>
+struct BwdlShape<true> {
+  static constexpr int threads = 64, minb = 7, warp_floats = PAIR_WARP_FLOATS;
+};
+template <>
+struct BwdlShape<false> {
+  static constexpr int threads = 128, minb = 4, warp_floats = BWD_WARP_FLOATS;
+};
+__device__ inline bool log_wants_pairs(const char* log) {
+  const LogHeader* h = (const LogHeader*)log;
+  return 16ull * h->pairs < (unsigned long long)GSX_BWDL_PAIR_MAX * h->entries;
+}
 
-__global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
+template <bool PAIRS>
+__global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::minb)
     k_render_backward_logged(SceneView sv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
                              int64_t tile_stride, BwdImages im, const char* __restrict__ log,
                              long long nw, float* __restrict__ grad) {
-  extern __shared__ __align__(16) float red_smem[];  // BWD_WARP_FLOATS per warp
-  const long long wid = tile_warp_id(BWDL_PER_TILE, BWDL_THREADS);
+  constexpr int NT = BwdlShape<PAIRS>::threads, PER_TILE = 256 / NT;
+  extern __shared__ __align__(16) float red_smem[];  // BwdlShape::warp_floats per warp
+  if (log_wants_pairs(log) != PAIRS) return;  // the other strategy's launch runs
+  const long long wid = tile_warp_id(PER_TILE, NT);
   if (!log_complete((void*)log, nw)[wid]) return;  // the replay kernel covers this warp
   const int lane = threadIdx.x & 31;
   RayCtx r;
   bool hit;
   int64_t pix;
-  const bool valid =
-      tile_pixel_ray(sv, cam, tile_begin, tile_stride, BWDL_PER_TILE, BWDL_THREADS, r, hit, pix);
+  const bool valid = tile_pixel_ray(sv, cam, tile_begin, tile_stride, PER_TILE, NT, r, hit, pix);
   const PixelGrad pg = pixel_grad(im, cfg, valid, pix);
   RayAccum acc;
   acc.init();
-  float Y[9];
-  sh_basis_f(r.df, Y);
-  float* wsm = red_smem + (threadIdx.x >> 5) * BWD_WARP_FLOATS;
-  GradBatch gb{wsm, wsm + RED_FLOATS, 0};
+  float* wsm = red_smem + (threadIdx.x >> 5) * BwdlShape<PAIRS>::warp_floats;
+  const PairBufs pb{wsm, wsm + PR_FLOATS, wsm + PR_FLOATS + WH_FLOATS};
+  GradBatch gb = PAIRS ? GradBatch{nullptr, wsm + PR_FLOATS + WH_FLOATS + LT_ROWS * 32, 0}
+                       : GradBatch{wsm, wsm + RED_FLOATS, 0};
+  float Y[PAIRS ? 1 : 9];
+  if constexpr (!PAIRS) sh_basis_f(r.df, Y);
   long long off = log_first((void*)log)[wid];
   while (off >= 0) {
     const long long start = off;
@@ -590,25 +867,50 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
     }
 #endif
     const SegBase base = seg_base(r, tb);
-    const bool want = mc > 0;
+    if constexpr (PAIRS) {
+      // the lane table and adjoints of this record for the pair lanes
+      float* lt = pb.lt + lane;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lt[k * 32] = r.df[k];
+        lt[(3 + k) * 32] = base.hi[k];
+        lt[(6 + k) * 32] = base.lo[k];
+        lt[(11 + k) * 32] = pg.gC[k];
+      }
+      lt[9 * 32] = dtf;
+      lt[10 * 32] = __int_as_float(mc);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        pb.wh[32 * j + lane] = wos[j];
+        pb.wh[512 + 32 * j + lane] = hh[j];
+      }
+      __syncwarp();
+    }
     // pass 2 over the record chain start..off
     for (long long o = start;;) {
       const LogRec* ho = (const LogRec*)(log + o);
       const int count = ho->count;
-      const int32_t* list = (const int32_t*)(log + o + 128 + (ho->kind == 0 ? Lo.list : 0));
-      for (int i0 = 0; i0 < count; i0 += 32) {
-        const int ent = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
-        const int nb = min(32, count - i0);
-        // (an L1 prefetch of entry k + 1 / k + 2's geometry and appearance
-        // measured slower: 13.15 vs 12.58 ms on C2)
-        for (int k = 0; k < nb; ++k) {
-          grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), want, mc, base, dtf, Y, pg,
-                         wos, hh, gb, grad);
+      const char* lb = log + o + 128;
+      const int32_t* list = (const int32_t*)(lb + (ho->kind == 0 ? Lo.list : 0));
+      if constexpr (PAIRS) {
+        const uint32_t* um =
+            (const uint32_t*)(lb + (ho->kind == 0 ? Lo.umask : log_chunk_umask(count)));
+        pair_pass(sv, pb, gb, list, um, count, grad);
+      } else {
+        for (int i0 = 0; i0 < count; i0 += 32) {
+          const int ent = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
+          const int nb = min(32, count - i0);
+          // (an L1 prefetch of entry k + 1 / k + 2's geometry and appearance
+          // measured slower: 13.15 vs 12.58 ms on C2)
+          for (int k = 0; k < nb; ++k)
+            grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), mc > 0, mc, base, dtf, Y,
+                           pg, wos, hh, gb, grad);
         }
       }
       if (o == off) break;
       o = ho->next;
     }
+    __syncwarp();
     off = next;
   }
   grad_batch_flush(sv, gb, grad);
@@ -617,15 +919,22 @@ __global__ void __launch_bounds__(BWDL_THREADS, GSX_BWDL_MINB)
 }  // namespace
 
 constexpr int BWD_SMEM = (BWD_THREADS / 32) * BWD_WARP_FLOATS * (int)sizeof(float);
-constexpr int BWDL_SMEM = (BWDL_THREADS / 32) * BWD_WARP_FLOATS * (int)sizeof(float);
+template <bool PAIRS>
+constexpr int bwdl_smem() {
+  return (BwdlShape<PAIRS>::threads / 32) * BwdlShape<PAIRS>::warp_floats * (int)sizeof(float);
+}
 
 static int bwd_smem_setup() {
   static bool done = false;  // idempotent; the attribute is per function
   if (done) return GSX_OK;
   if (cudaFuncSetAttribute(k_render_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            BWD_SMEM) != cudaSuccess ||
-      cudaFuncSetAttribute(k_render_backward_logged,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, BWDL_SMEM) != cudaSuccess)
+      cudaFuncSetAttribute(k_render_backward_logged<true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           bwdl_smem<true>()) != cudaSuccess ||
+      cudaFuncSetAttribute(k_render_backward_logged<false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           bwdl_smem<false>()) != cudaSuccess)
     return gsx_check_launch();
   done = true;
   return GSX_OK;
@@ -690,7 +999,11 @@ extern "C" int gsx_render_backward_logged(const void* scene_arena, const void* b
   cudaStream_t s = (cudaStream_t)stream;
   rc = bwd_smem_setup();
   if (rc) return rc;
-  k_render_backward_logged<<<(unsigned)(BWDL_PER_TILE * ntl), BWDL_THREADS, BWDL_SMEM, s>>>(
+  k_render_backward_logged<true><<<(unsigned)(256 / BwdlShape<true>::threads * ntl),
+                                   BwdlShape<true>::threads, bwdl_smem<true>(), s>>>(
+      sv, *cam, *cfg, tile_begin, tile_stride, im, (const char*)log, nw, grad);
+  k_render_backward_logged<false><<<(unsigned)(256 / BwdlShape<false>::threads * ntl),
+                                    BwdlShape<false>::threads, bwdl_smem<false>(), s>>>(
       sv, *cam, *cfg, tile_begin, tile_stride, im, (const char*)log, nw, grad);
   // warps whose records overflowed the arena: full replay
   k_render_backward<<<(unsigned)(BWD_PER_TILE * ntl), BWD_THREADS, BWD_SMEM, s>>>(

@@ -682,8 +682,9 @@ __device__ inline CandUse candidate_use(const SceneView& sv, const RayCtx& r, in
 
 // Pass-1 accumulation of one candidate into the 16 per-sample sums
 // (renderer.py:218-228), given its setup.
+// Returns the lanes that set p up (0 if none; the logged forward stores it).
 template <class L = LdgLoad, int CH = 16, class YT = const float*>
-__device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, const CandUse& u,
+__device__ inline unsigned accumulate_used_at(const float4* app, const RayCtx& r, const CandUse& u,
                                           float dtf, YT Y, float (&sig)[CH],
                                           float (&W)[CH][3]) {
   const CandSetup& cs = u.cs;
@@ -691,7 +692,8 @@ __device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, co
   const int jlo = u.jlo, jhi = u.jhi;
   PH_CNT(9, 1)
   PH_LANES(11, use)
-  if (!__any_sync(FULL, use)) return false;
+  const unsigned um = __ballot_sync(FULL, use);
+  if (!um) return 0u;
   PH_CNT(14, 1)
   float c[3] = {0.f, 0.f, 0.f};
   if (use) eval_radiance_f<L, YT>(app, Y, r.df, c);
@@ -715,18 +717,18 @@ __device__ inline bool accumulate_used_at(const float4* app, const RayCtx& r, co
       }
     }
   }
-  return true;
+  return um;
 }
 
 template <int CH, class YT>
-__device__ inline bool accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
+__device__ inline unsigned accumulate_used(const SceneView& sv, const RayCtx& r, int64_t p,
                                        const CandUse& u, float dtf, YT Y,
                                        float (&sig)[CH], float (&W)[CH][3]) {
   return accumulate_used_at(sv.app + GSX_APP_F4 * p, r, u, dtf, Y, sig, W);
 }
 
 template <int CH, class YT>
-__device__ inline bool accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
+__device__ inline unsigned accumulate_candidate(const SceneView& sv, const RayCtx& r, int64_t p,
                                             bool want, int mc, const SegBase& base, float dtf,
                                             YT Y, float (&sig)[CH],
                                             float (&W)[CH][3]) {
@@ -738,22 +740,26 @@ __device__ inline bool accumulate_candidate(const SceneView& sv, const RayCtx& r
 // setups for ILP measured slower: the extra live state spills at 128 regs.)
 // COMPACT: the list is compacted in place to the entries some lane used (the
 // only ones with a non-zero contribution, hence the only ones the logged
-// backward needs); returns the new count.
+// backward needs) and their lanes' masks go to umask[0, count); returns the
+// new count.
 template <bool COMPACT = false, class Pre, int CH, class YT>
 __device__ inline int accumulate_list(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
                                       int count, bool want, int mc, const SegBase& base,
                                       float dtf, YT Y, float (&sig)[CH],
-                                      float (&W)[CH][3], Pre&& pre) {
+                                      float (&W)[CH][3], uint32_t* umask, Pre&& pre) {
   // (L1 prefetch of the listed geometry / appearance blocks measured slower:
   // 40.9 vs 40.0 ms on C3 -- the entry loop is not load-latency bound)
   int kept = 0;
   for (int i = 0; i < count; ++i) {
     const int64_t p = sm.list[i];
     pre(p, want);
-    const bool used = accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
+    const unsigned used = accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
     if (COMPACT && used) {
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) sm.list[kept] = (int32_t)p;
+      if ((threadIdx.x & 31) == 0) {
+        sm.list[kept] = (int32_t)p;
+        umask[kept] = used;
+      }
       ++kept;
     }
   }
@@ -789,11 +795,14 @@ struct Screen {
 #ifndef GSX_SCR_CH
 #define GSX_SCR_CH 16
 #endif
-struct WarpSmemR : WarpSmem {  // screened forward, sums in registers
+struct WarpSmemR : WarpSmem {  // screen masks (the unscreened training forward: use masks)
   uint32_t mask[LCAP];
 };
+struct WarpSmemL : WarpSmemR {  // screened training forward: + the use masks of the kept entries
+  uint32_t umask[LCAP];
+};
 template <int CH>
-struct WarpSmemS : WarpSmemR {  // screened training forward, sums in shared memory
+struct WarpSmemS : WarpSmemL {  // screened training forward, sums in shared memory
   float4 acc[CH][32];
 };
 template <int CH>
@@ -875,10 +884,6 @@ __device__ inline void screen_list(const Screen& sc, WarpSmemR& sm, int count, u
 // clearly inside an ellipsoid (q <= 0.998 in fp32): that sample is then
 // inside the primitive's fp64 AABB too, so the segment is AABB-non-empty in
 // the reference's sense (spatial.py:234-241) without the exact slab test.
-// COMPACT (logged forward): the entries some lane used -- the only ones the
-// logged backward needs -- are also written, in list order, over the
-// already-consumed front of sm.mask (read back as int32); returns their
-// count.  sm.list stays whole for the exact emptiness test.
 // Samples of one set-up entry into the lane's shared-memory column (the
 // 4-sample groups outside every lane's range skipped warp-uniformly); q <= 1
 // decides exactly, as in accumulate_used_at.  Returns the lane's smallest
@@ -915,10 +920,11 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
 // loop body doubles.)
 // COMPACT (logged forward): the entries some lane used -- the only ones the
 // logged backward needs -- are also written, in list order, over the
-// already-consumed front of sm.mask (read back as int32); returns their
-// count.  sm.list stays whole for the exact emptiness test.
+// already-consumed front of sm.mask (read back as int32), and the lanes that
+// used them to sm.umask; returns their count.  sm.list stays whole for the
+// exact emptiness test.
 template <int CH, bool COMPACT = false, class YT, class Sums>
-__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemR& sm,
+__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemL& sm,
                                           int count, bool want, int mc, const SegBase& base,
                                           float dtf, YT Y, Sums& sums, bool& inside) {
   int kept = 0;
@@ -929,9 +935,13 @@ __device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, 
     if (m == 0u) continue;
     const int64_t p = sm.list[i];
     const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
-    if (!__any_sync(FULL, u.use)) continue;
+    const unsigned um = __ballot_sync(FULL, u.use);
+    if (!um) continue;
     if (COMPACT) {
-      if (lane == 0) sm.mask[kept] = (uint32_t)p;  // kept <= i: masks ahead are intact
+      if (lane == 0) {
+        sm.mask[kept] = (uint32_t)p;  // kept <= i: masks ahead are intact
+        sm.umask[kept] = um;
+      }
       ++kept;
     }
     float c[3] = {0.f, 0.f, 0.f};
