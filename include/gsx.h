@@ -268,9 +268,12 @@ int gsx_render_backward(const void* scene_arena, const void* bvh_arena, const fl
                         gsx_dev_status* dev_status, void* stream);
 
 /* ---- march log (training; no reference counterpart) --------------------------
- * A training forward can record, per warp, the candidate lists and per-sample
- * sums it computes into a device arena (`log`, log_bytes); the logged backward
- * then skips the replay traversal and density pass.  Warps whose records do
+ * A training forward can record, per warp, the candidate lists (with the mask
+ * of lanes that used each entry) and per-sample sums it computes into a
+ * device arena (`log`, log_bytes); the logged backward then skips the replay
+ * traversal and density pass, and picks its pass-2 strategy (all lanes per
+ * entry, or compacted (lane, primitive) pairs) on the device from the log's
+ * lanes-per-entry statistics.  Warps whose records do
  * not fit are flagged and replayed by gsx_render_backward's kernel inside
  * gsx_render_backward_logged, so any capacity >= gsx_march_log_min_bytes is
  * correct; gsx_march_log_usage (synchronizes `stream`) reports the bytes the
