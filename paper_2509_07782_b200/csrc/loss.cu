@@ -15,6 +15,9 @@
 // K9 restates geometry.py:193-233 (ratio_upper_bound, isotropic_loss) and
 // accumulates lambda_s * dL_s/ds into the record gradient (scales clamped at
 // S_MIN receive none).
+#include <algorithm>
+#include <climits>
+#include <cstdint>
 #include "gsx_common.cuh"
 
 namespace {
@@ -221,22 +224,59 @@ __global__ void k_iso_loss(const float* __restrict__ params, int64_t n, double r
 }
 
 // ---- fused Adam over the [N, 87] records -----------------------------------------
-__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                       float* __restrict__ v, int64_t count, const float* __restrict__ lr87,
-                       const float* __restrict__ lo87, float b1, float b2, float eps, float bc1,
-                       float bc2) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  float gi = g[i];
-  float mi = fmaf(b1, m[i], (1.f - b1) * gi);
-  float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
-  m[i] = mi;
-  v[i] = vi;
-  const int slot = (int)(i % GSX_NREC);
-  float np_ = p[i] - lr87[slot] * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+// HBM-bound: 16 B read (p, g, m, v) + 12 B written (p, m, v) per value.  One
+// float4 of each stream per thread (grid-stride loop for very large N); the
+// record slot (value index mod 87) is carried across iterations.
+struct AdamArgs {
+  const float* lr87;
+  const float* lo87;
+  float b1, b2, eps, bc1, bc2;
+};
+__device__ __forceinline__ float adam_one(float& pi, float gi, float& mi, float& vi, int slot,
+                                          const AdamArgs& a) {
+  mi = fmaf(a.b1, mi, (1.f - a.b1) * gi);
+  vi = fmaf(a.b2, vi, (1.f - a.b2) * gi * gi);
+  const float np_ = pi - __ldg(a.lr87 + slot) * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
   // projection onto the record's validity domain (sigma~ > sigma_eps,
   // scales > 0, sharpness >= 0): lo87 = per-slot lower bound (-inf = none)
-  p[i] = fmaxf(np_, lo87[slot]);
+  pi = fmaxf(np_, __ldg(a.lo87 + slot));
+  return pi;
+}
+__global__ void __launch_bounds__(256) k_adam4(float4* __restrict__ p, const float4* __restrict__ g,
+                                               float4* __restrict__ m, float4* __restrict__ v,
+                                               int64_t n4, AdamArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n4) return;
+  int slot = (int)((4 * q) % GSX_NREC);
+  const int step = (int)((4 * stride) % GSX_NREC);
+  for (; q < n4; q += stride) {
+    float4 pp = p[q], mm = m[q], vv = v[q];
+    const float4 gg = __ldcs(g + q);
+    const int s1 = slot + 1 - (slot + 1 >= GSX_NREC ? GSX_NREC : 0);
+    const int s2 = s1 + 1 - (s1 + 1 >= GSX_NREC ? GSX_NREC : 0);
+    const int s3 = s2 + 1 - (s2 + 1 >= GSX_NREC ? GSX_NREC : 0);
+    adam_one(pp.x, gg.x, mm.x, vv.x, slot, a);
+    adam_one(pp.y, gg.y, mm.y, vv.y, s1, a);
+    adam_one(pp.z, gg.z, mm.z, vv.z, s2, a);
+    adam_one(pp.w, gg.w, mm.w, vv.w, s3, a);
+    p[q] = pp;
+    m[q] = mm;
+    v[q] = vv;
+    slot += step;
+    slot -= slot >= GSX_NREC ? GSX_NREC : 0;
+  }
+}
+// scalar tail / unaligned views (a row shard of the padded parameters)
+__global__ void k_adam1(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                        float* __restrict__ v, int64_t begin, int64_t count, AdamArgs a) {
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float pi = p[i], mi = m[i], vi = v[i];
+  adam_one(pi, g[i], mi, vi, (int)(i % GSX_NREC), a);
+  p[i] = pi;
+  m[i] = mi;
+  v[i] = vi;
 }
 
 }  // namespace
@@ -301,8 +341,23 @@ extern "C" int gsx_adam_step(float* params, const float* grad, float* m, float* 
                              double eps, int64_t step, void* stream) {
   if (n <= 0 || step < 1) return GSX_ERR_ARG;
   int64_t count = n * GSX_NREC;
-  float bc1 = (float)(1.0 - pow(beta1, (double)step)), bc2 = (float)(1.0 - pow(beta2, (double)step));
-  k_adam<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      params, grad, m, v, count, lr87, lo87, (float)beta1, (float)beta2, (float)eps, bc1, bc2);
+  const AdamArgs a{lr87, lo87, (float)beta1, (float)beta2, (float)eps,
+                   (float)(1.0 - pow(beta1, (double)step)), (float)(1.0 - pow(beta2, (double)step))};
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t done = 0;
+  if ((((uintptr_t)params | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) == 0) {
+    const int64_t n4 = count / 4;
+    if (n4 > 0) {
+      // one float4 per thread (a grid-stride loop over 8 CTAs per SM measured
+      // 1.93 vs 1.89 ms for the 3M-record C4 step; ~3.8 TB/s either way)
+      const int64_t blocks = std::min<int64_t>((n4 + 255) / 256, (int64_t)INT32_MAX);
+      k_adam4<<<(unsigned)blocks, 256, 0, s>>>((float4*)params, (const float4*)grad, (float4*)m,
+                                               (float4*)v, n4, a);
+      done = 4 * n4;
+    }
+  }
+  if (done < count)
+    k_adam1<<<(unsigned)((count - done + 255) / 256), 256, 0, s>>>(params, grad, m, v, done,
+                                                                   count, a);
   return gsx_check_launch();
 }

@@ -17,13 +17,15 @@
 // lanes waiting in most iterations) are stored, in slot order
 // slot = popc(act & lanes below):
 //   kind 0 (full):  double tb[nact], double dt[nact], int32 mc[nact],
-//                   float4 smp[mmax][nact] (sigma, W0, W1, W2), int32 list[count],
-//                   uint32 umask[count] (each array 16-byte aligned, see LogLayout)
-//   kind 1 (list):  int32 list[count], uint32 umask[count]  (a leading chunk of
+//                   float4 smp[mmax][nact] (sigma, W0, W1, W2), int32 list[cap],
+//                   uint32 umask[cap] (each array 16-byte aligned, see LogLayout)
+//   kind 1 (list):  int32 list[cap], uint32 umask[cap]  (a leading chunk of
 //                   a candidate stream longer than the shared list; the kind-0
 //                   record that follows holds the rest and the sample sums)
-// umask[i] = the lanes (bit = lane) whose setup of list[i] succeeded in the
-// forward: exactly the (lane, primitive) pairs the backward's pass 2 visits.
+// The arrays are sized for the traversed list (cap entries) and hold its
+// first `count` entries that some lane used, in list order; umask[i] = those
+// lanes (bit = lane): exactly the (lane, primitive) pairs the backward's
+// pass 2 visits.
 // A warp whose records did not fit (bump pointer past capacity) is marked
 // complete = 0 and the backward recomputes it with the replay kernel.
 #pragma once
@@ -37,7 +39,7 @@ struct LogHeader {
   unsigned int overflow;
   unsigned int nwarps;
   unsigned long long need;  // bytes every record would need (incl. those that did not fit)
-  unsigned long long entries, pairs;  // logged list entries, sum of their use-mask popcounts
+  unsigned long long entries, pairs;  // logged entries some lane used, sum of their mask popcounts
   unsigned int pad[20];
 };
 static_assert(sizeof(LogHeader) == 128, "LogHeader is one 128-byte line");
@@ -48,7 +50,8 @@ struct LogRec {
   int kind;        // 0 full, 1 list chunk
   int mmax;        // samples stored per active lane (warp max of mc), kind 0
   unsigned act;    // lanes stored (mc > 0), kind 0
-  int pad[26];
+  int cap;         // entries the list / umask arrays were sized for (>= count)
+  int pad[25];
 };
 static_assert(sizeof(LogRec) == 128, "LogRec is one 128-byte line");
 
@@ -137,12 +140,13 @@ __device__ inline long long log_alloc(LogWriter& w, long long bytes) {
   return off;
 }
 
-__device__ inline void log_header(const LogWriter& w, long long off, int count, int kind,
+__device__ inline void log_header(const LogWriter& w, long long off, int cap, int kind,
                                   int mmax, unsigned act) {
   if ((threadIdx.x & 31) == 0) {
     LogRec* r = (LogRec*)(w.base + off);
     r->next = -1;
-    r->count = count;
+    r->count = 0;  // log_close
+    r->cap = cap;
     r->kind = kind;
     r->mmax = mmax;
     r->act = act;
@@ -151,99 +155,97 @@ __device__ inline void log_header(const LogWriter& w, long long off, int count, 
 
 // The log streams through L2 once each way: evict-first stores/loads keep
 // the scene and BVH resident.
-__device__ inline void log_list(LogWriter& w, int32_t* dst, const int32_t* list, uint32_t* mdst,
-                                const uint32_t* umask, int count) {
-  for (int i = threadIdx.x & 31; i < count; i += 32) {
-    const uint32_t m = umask[i];
-    __stcs(dst + i, list[i]);
-    __stcs(mdst + i, m);
-    w.entries += 1u;
-    w.pairs += (unsigned)__popc(m);
+//
+// A record is opened right after the traversal that produced its list (its
+// entry count is the record's capacity; whether it is the chunk's last list
+// -- kind 0, with the lane block and, at the end of the chunk, the sample
+// sums -- or a leading kind-1 chunk is known then too).  The accumulation
+// appends the entries some lane used, with their masks, straight into the
+// record (log_keep) and log_close sets the count, so the forward needs no
+// shared-memory compaction arrays.
+
+// The open record of the current list (all null: not logged / overflow).
+struct LogRecPtrs {
+  LogRec* hdr;
+  int32_t* list;
+  uint32_t* umask;
+  float4* smp;  // this lane's first sample-sum slot (kind 0, lanes with samples)
+  int nact, mmax;
+};
+
+// Warp-uniform.  final: the chunk's last list (kind 0, lane block written
+// here: tb, dt, this lane's sample count mc); else a kind-1 list chunk.
+__device__ inline LogRecPtrs log_open(LogWriter& w, int count, bool final, double tb,
+                                      double dt, int mc) {
+  LogRecPtrs o{nullptr, nullptr, nullptr, nullptr, 0, 0};
+  if (!w.base) return o;
+  if (!final) {
+    const long long off = log_alloc(w, log_chunk_bytes(count));
+    if (off < 0) return o;
+    log_header(w, off, count, 1, 0, 0u);
+    char* body = w.base + off + 128;
+    o.hdr = (LogRec*)(w.base + off);
+    o.list = (int32_t*)body;
+    o.umask = (uint32_t*)(body + log_chunk_umask(count));
+    return o;
   }
-}
-
-// The record writers run once per warp iteration inside the march loop; kept
-// out of line (GSX_LOG_OOL) they stay out of the hot loop's instruction
-// footprint, and only the per-lane sample-sum stores remain inline.
-#ifndef GSX_LOG_OOL
-#define GSX_LOG_OOL 0
-#endif
-#if GSX_LOG_OOL
-#define GSX_LOG_ATTR __noinline__
-#else
-#define GSX_LOG_ATTR inline
-#endif
-
-// kind 1: a full shared-list chunk of a long candidate stream
-__device__ GSX_LOG_ATTR void log_list_chunk(LogWriter& w, const int32_t* list,
-                                            const uint32_t* umask, int count) {
-  if (!w.base) return;
-  const long long off = log_alloc(w, log_chunk_bytes(count));
-  if (off < 0) return;
-  log_header(w, off, count, 1, 0, 0u);
-  char* body = w.base + off + 128;
-  log_list(w, (int32_t*)body, list, (uint32_t*)(body + log_chunk_umask(count)), umask, count);
-}
-
-// kind 0 without the sample sums: allocates the record, writes its header,
-// the lane block (tb, dt, mc) and the list; returns the lane's first
-// sample-sum slot (nullptr for lanes without samples or on overflow) and the
-// warp-uniform stride nact / row count mmax of the sample-sum array.
-__device__ GSX_LOG_ATTR float4* log_full_head(LogWriter& w, const int32_t* list,
-                                              const uint32_t* umask, int count, double tb,
-                                              double dt, int mc, int& nact_out, int& mmax_out) {
   const int lane = threadIdx.x & 31;
   const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
   const int nact = __popc(act);
-  const int mmax = __reduce_max_sync(0xffffffffu, (unsigned)mc);
-  nact_out = nact;
-  mmax_out = 0;
+  const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mc > 0 ? mc : 0));
   const LogLayout L(nact, mmax, count);
   const long long off = log_alloc(w, L.bytes);
-  if (off < 0) return nullptr;
-  mmax_out = mmax;
+  if (off < 0) return o;
   log_header(w, off, count, 0, mmax, act);
   char* body = w.base + off + 128;
-  log_list(w, (int32_t*)(body + L.list), list, (uint32_t*)(body + L.umask), umask, count);
-  if (mc <= 0) return nullptr;
-  const int slot = __popc(act & ((1u << lane) - 1u));
-  __stcs((double*)body + slot, tb);
-  __stcs((double*)(body + L.dt) + slot, dt);
-  __stcs((int*)(body + L.mc) + slot, mc);
-  return (float4*)(body + L.smp) + slot;
+  o.hdr = (LogRec*)(w.base + off);
+  o.list = (int32_t*)(body + L.list);
+  o.umask = (uint32_t*)(body + L.umask);
+  o.nact = nact;
+  o.mmax = mmax;
+  if (mc > 0) {
+    const int slot = __popc(act & ((1u << lane) - 1u));
+    __stcs((double*)body + slot, tb);
+    __stcs((double*)(body + L.dt) + slot, dt);
+    __stcs((int*)(body + L.mc) + slot, mc);
+    o.smp = (float4*)(body + L.smp) + slot;
+  }
+  return o;
 }
 
-// kind 0: the active lanes' block, their per-sample sums, the last list chunk
-__device__ inline void log_full(LogWriter& w, const int32_t* list, const uint32_t* umask,
-                                int count, double tb, double dt, int mc,
-                                const float (&sig)[16], const float (&W)[16][3]) {
-  if (!w.base) return;
-  int nact, mmax;
-  float4* smp = log_full_head(w, list, umask, count, tb, dt, mc, nact, mmax);
-  if (smp) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j < mmax)
-        __stcs(smp + (long long)j * nact,
-               j < mc ? make_float4(sig[j], W[j][0], W[j][1], W[j][2])
-                      : make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-  }
+// The same out of line: keeps the record set-up out of the hot loop's
+// instruction footprint.  C2 logged forward, shared-memory-sum kernel: 17.1
+// vs 17.8 ms (its instruction-cache misses: no_instruction stalls 1.9 -> 0.8
+// warps per issue); the 64-register kernels are faster with it inline
+// (C4 register-sum 28.2 vs 29.4 ms).
+static __device__ __noinline__ LogRecPtrs log_open_ool(LogWriter& w, int count, bool final,
+                                                       double tb, double dt, int mc) {
+  return log_open(w, count, final, tb, dt, mc);
 }
 
-// kind 0 from the screened forward's sums (sums.get(j) = (sigma_j, W_j))
-template <class Sums>
-__device__ inline void log_full_sums(LogWriter& w, const int32_t* list, const uint32_t* umask,
-                                     int count, double tb, double dt, int mc, const Sums& sums) {
-  if (!w.base) return;
-  int nact, mmax;
-  float4* smp = log_full_head(w, list, umask, count, tb, dt, mc, nact, mmax);
-  if (smp) {
+// kept entry k of the open record: primitive p and the lanes um that used it
+// (called by the one lane holding the entry)
+__device__ inline void log_keep(LogWriter& w, const LogRecPtrs& o, int k, int32_t p,
+                                uint32_t um) {
+  if (!o.list) return;
+  __stcs(o.list + k, p);
+  __stcs(o.umask + k, um);
+  w.entries += 1u;
+  w.pairs += (unsigned)__popc(um);
+}
+// warp-uniform: the record holds `kept` entries
+__device__ inline void log_close(const LogRecPtrs& o, int kept) {
+  if (o.hdr && (threadIdx.x & 31) == 0) o.hdr->count = kept;
+}
+
+// kind 0: this lane's per-sample sums (get(j) = (sigma_j, W_j)) of the chunk
+template <class Get>
+__device__ inline void log_samples(const LogRecPtrs& o, int mc, Get&& get) {
+  if (!o.smp) return;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < mmax)
-        __stcs(smp + (long long)j * nact, j < mc ? sums.get(j) : make_float4(0.f, 0.f, 0.f, 0.f));
-  }
+  for (int j = 0; j < 16; ++j)
+    if (j < o.mmax)
+      __stcs(o.smp + (long long)j * o.nact, j < mc ? get(j) : make_float4(0.f, 0.f, 0.f, 0.f));
 }
 
 // end of the warp: publish its chain head and whether it is complete

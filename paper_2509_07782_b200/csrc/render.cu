@@ -90,10 +90,6 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
   constexpr int CH = SAVE ? 16 : GSX_FWD_CH;
   const int nchunks = (ns + CH - 1) / CH;
   uint32_t visits = 0;
-  // the training forward's smem is a WarpSmemR: its mask array takes the
-  // kept entries' use masks (k_render_camera)
-  uint32_t* umask = nullptr;
-  if constexpr (SAVE) umask = static_cast<WarpSmemR&>(sm).mask;
   for (int ch = 0; ch < nchunks; ++ch) {
     int mc = want ? seg.m - ch * CH : 0;
     mc = mc < 0 ? 0 : (mc > CH ? CH : mc);
@@ -134,6 +130,7 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       if (!STATS && gate && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
     };
+    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0};
     for (;;) {
       PH_BEGIN(ph_t)
       if (CONE)
@@ -141,19 +138,27 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       else
         warp_traverse(bv, r, wch, lim.lo_t, lim.hi_t, lim.gap, st, sm, count, visits);
       PH_END(1, ph_t)
+      const bool last = CONE ? cst.done : st.done;
+      if constexpr (SAVE) {
+        if (save) lo = log_open(lw, count, last, tb, seg.dt, mc);
+      }
       PH_BEGIN(ph_p)
-      // the logged forward records only the entries some lane used
-      count = accumulate_list<SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, umask,
-                                    exact);
+      int kept = 0;  // logged forward: the entries some lane used, in list order
+      accumulate_list(sv, r, sm, count, wch, mc, base, dtf, Y, sig, W, exact,
+                      [&](int, int64_t p, unsigned um) {
+                        if (SAVE && um) {
+                          if ((threadIdx.x & 31) == 0) log_keep(lw, lo, kept, (int32_t)p, um);
+                          ++kept;
+                        }
+                      });
+      if constexpr (SAVE) log_close(lo, kept);
       PH_END(2, ph_p)
-      if (CONE ? cst.done : st.done) break;
-      if (save) log_list_chunk(lw, sm.list, umask, count);
+      if (last) break;
       __syncwarp();
       count = 0;
     }
-    if constexpr (SAVE) {
-      if (save) log_full(lw, sm.list, umask, count, tb, seg.dt, mc, sig, W);
-    }
+    if constexpr (SAVE)
+      log_samples(lo, mc, [&](int j) { return make_float4(sig[j], W[j][0], W[j][1], W[j][2]); });
     if (STATS) {
 #pragma unroll
       for (int j = 0; j < CH; ++j) cnt.composited += (j < mc && sig[j] > 0.f) ? 1u : 0u;
@@ -289,8 +294,7 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
     SceneView sv, BvhView bv, gsx_camera cam, gsx_render_cfg cfg, int64_t tile_begin,
     int64_t tile_stride, float* rgb, float* depth, float* trans, gsx_stats* stats, void* log,
     long long log_nw) {
-  using WS = std::conditional_t<SAVE, WarpSmemR, WarpSmem>;
-  __shared__ WS smem[NT / 32];
+  __shared__ WarpSmem smem[NT / 32];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
   render_warp_block<STATS, SAVE, CONE>(sv, bv, cam, cfg, tile_begin, tile_stride, blk, rgb, depth,
                                  trans, stats, log, log_nw, smem[threadIdx.x >> 5]);
@@ -299,7 +303,8 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
 // ---------------------------------------------------------------------------
 // Screened plain forward (the benchmarked frame): the camera kernel above
 // with the per-camera silhouette screen (Screen, render_warp.cuh) in front of
-// every list and the per-sample sums in shared memory (WarpSmemS).  Same
+// every list and the per-sample sums in shared memory (WarpSmemA) or
+// registers.  Same
 // march, same per-lane arithmetic in the same order: its pixels equal the
 // unscreened kernel's bit for bit.
 // ---------------------------------------------------------------------------
@@ -339,17 +344,26 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     cone_begin(sm, cst);
     const unsigned lanes = __ballot_sync(FULL, wch && mc > 0);
     const bool save = SAVE && __any_sync(FULL, want && mc > 0);
-    int count = 0, kept = 0;
+    int count = 0;
+    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0};
     for (;;) {
       warp_traverse_cone(bv, cst, sm, count, visits);
-      bool inside = false;
       if constexpr (SAVE) {
-        screen_list(sc, sm, count, lanes);
-        kept = accumulate_screened<CH, SAVE>(sv, r, sm, count, wch, mc, base, dtf, Y, sums,
-                                             inside);
-      } else {
-        screen_accumulate<CH>(sc, sv, r, sm, count, lanes, wch, mc, base, dtf, Y, sums, inside);
+        if (save)
+          lo = SMEM ? log_open_ool(lw, count, cst.done, tb, seg.dt, mc)
+                    : log_open(lw, count, cst.done, tb, seg.dt, mc);
       }
+      bool inside = false;
+      int kept = 0;  // logged forward: the entries some lane used, in list order
+      screen_accumulate<CH>(sc, sv, r, sm, count, lanes, wch, mc, base, dtf, Y, sums, inside,
+                            [&](int32_t p, unsigned um) {
+                              if constexpr (SAVE) {
+                                const unsigned kb = __ballot_sync(FULL, um != 0u);
+                                if (um) log_keep(lw, lo, kept + __popc(kb & lanemask_lt()), p, um);
+                                kept += __popc(kb);
+                              }
+                            });
+      if constexpr (SAVE) log_close(lo, kept);
       nonempty = nonempty || inside;
       // AABB emptiness without a clearly-inside sample: the exact test over
       // this chunk of the list (a superset of the boxes the segment meets)
@@ -361,15 +375,9 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
           }
       __syncwarp();
       if (cst.done) break;
-      if constexpr (SAVE) {
-        if (save) log_list_chunk(lw, (const int32_t*)sm.mask, sm.umask, kept);
-      }
-      __syncwarp();
       count = 0;
     }
-    if constexpr (SAVE) {
-      if (save) log_full_sums(lw, (const int32_t*)sm.mask, sm.umask, kept, tb, seg.dt, mc, sums);
-    }
+    if constexpr (SAVE) log_samples(lo, mc, [&](int j) { return sums.get(j); });
     // front-to-back compositing (renderer.py:230-239)
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -407,10 +415,7 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
                       int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
                       float* trans, const float4* view, void* log, long long log_nw) {
   constexpr int CH = GSX_SCR_CH;
-  // the training forward keeps the mask array (its used-entry compaction
-  // writes into it); the plain forward screens batch by batch in registers
-  using WS = std::conditional_t<SAVE, std::conditional_t<SMEM, WarpSmemS<CH>, WarpSmemL>,
-                                std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmem>>;
+  using WS = std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmem>;
   __shared__ WS smem[NT / 32];
   WS& sw = smem[threadIdx.x >> 5];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);

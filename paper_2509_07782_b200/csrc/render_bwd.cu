@@ -357,7 +357,8 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
         if (want && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1)) nonempty = true;
       };
       for (;;) {
-        accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, nullptr, exact);
+        accumulate_list(sv, r, sm, count, want, mc, base, dtf, Y, sig, W, exact,
+                        [](int, int64_t, unsigned) {});
         if (st.done) break;
         __syncwarp();
         count = 0;
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
     const unsigned act = h->act;
     const int mmax = h->mmax;
     const long long next = h->next;
-    const LogLayout Lo(__popc(act), mmax, h->count);
+    const LogLayout Lo(__popc(act), mmax, h->cap);
     if (next >= 0) log_prefetch(log + next, 128 + Lo.list);
     const bool mine = (act >> lane) & 1u;
     const int slot = __popc(act & ((1u << lane) - 1u));
@@ -892,9 +893,9 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
       const int count = ho->count;
       const char* lb = log + o + 128;
       const int32_t* list = (const int32_t*)(lb + (ho->kind == 0 ? Lo.list : 0));
+      const uint32_t* um =
+          (const uint32_t*)(lb + (ho->kind == 0 ? Lo.umask : log_chunk_umask(ho->cap)));
       if constexpr (PAIRS) {
-        const uint32_t* um =
-            (const uint32_t*)(lb + (ho->kind == 0 ? Lo.umask : log_chunk_umask(count)));
         pair_pass(sv, pb, gb, list, um, count, grad);
       } else {
         for (int i0 = 0; i0 < count; i0 += 32) {

@@ -738,33 +738,20 @@ __device__ inline unsigned accumulate_candidate(const SceneView& sv, const RayCt
 
 // Pass 1 over a staged list in list order.  (Interleaving two candidates'
 // setups for ILP measured slower: the extra live state spills at 128 regs.)
-// COMPACT: the list is compacted in place to the entries some lane used (the
-// only ones with a non-zero contribution, hence the only ones the logged
-// backward needs) and their lanes' masks go to umask[0, count); returns the
-// new count.
-template <bool COMPACT = false, class Pre, int CH, class YT>
-__device__ inline int accumulate_list(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
-                                      int count, bool want, int mc, const SegBase& base,
-                                      float dtf, YT Y, float (&sig)[CH],
-                                      float (&W)[CH][3], uint32_t* umask, Pre&& pre) {
+// post(i, p, lanes that used entry i) after each entry (warp-uniform; the
+// logged forward records it).
+template <class Pre, class Post, int CH, class YT>
+__device__ inline void accumulate_list(const SceneView& sv, const RayCtx& r, WarpSmem& sm,
+                                       int count, bool want, int mc, const SegBase& base,
+                                       float dtf, YT Y, float (&sig)[CH], float (&W)[CH][3],
+                                       Pre&& pre, Post&& post) {
   // (L1 prefetch of the listed geometry / appearance blocks measured slower:
   // 40.9 vs 40.0 ms on C3 -- the entry loop is not load-latency bound)
-  int kept = 0;
   for (int i = 0; i < count; ++i) {
     const int64_t p = sm.list[i];
     pre(p, want);
-    const unsigned used = accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W);
-    if (COMPACT && used) {
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) {
-        sm.list[kept] = (int32_t)p;
-        umask[kept] = used;
-      }
-      ++kept;
-    }
+    post(i, p, accumulate_candidate(sv, r, p, want, mc, base, dtf, Y, sig, W));
   }
-  if (COMPACT) __syncwarp();
-  return COMPACT ? kept : count;
 }
 
 
@@ -795,18 +782,8 @@ struct Screen {
 #ifndef GSX_SCR_CH
 #define GSX_SCR_CH 16
 #endif
-struct WarpSmemR : WarpSmem {  // screen masks (the unscreened training forward: use masks)
-  uint32_t mask[LCAP];
-};
-struct WarpSmemL : WarpSmemR {  // screened training forward: + the use masks of the kept entries
-  uint32_t umask[LCAP];
-};
 template <int CH>
-struct WarpSmemS : WarpSmemL {  // screened training forward, sums in shared memory
-  float4 acc[CH][32];
-};
-template <int CH>
-struct WarpSmemA : WarpSmem {  // screened plain forward, sums in shared memory
+struct WarpSmemA : WarpSmem {  // screened forward, sums in shared memory
   float4 acc[CH][32];
 };
 
@@ -868,23 +845,12 @@ __device__ inline unsigned screen_entry(const Screen& sc, int64_t p) {
   return m;
 }
 
-__device__ inline void screen_list(const Screen& sc, WarpSmemR& sm, int count, unsigned lanes) {
-  const unsigned lane = threadIdx.x & 31;
-  for (int b = 0; b < count; b += 32) {
-    const int i = b + (int)lane;
-    if (i < count) sm.mask[i] = screen_entry(sc, sm.list[i]) & lanes;
-  }
-  __syncwarp();
-}
-
-// Pass 1 over a screened list: entries no lane can use are skipped
-// warp-uniformly, and a lane sets up only the entries whose mask holds it;
-// the sums go to the lane's shared-memory column acc[j][lane] (one 16-byte
-// load / store per updated sample).  `inside` is set when a sample lies
+// Screened pass 1 (screen_accumulate): `inside` is set when a sample lies
 // clearly inside an ellipsoid (q <= 0.998 in fp32): that sample is then
 // inside the primitive's fp64 AABB too, so the segment is AABB-non-empty in
 // the reference's sense (spatial.py:234-241) without the exact slab test.
-// Samples of one set-up entry into the lane's shared-memory column (the
+//
+// Samples of one set-up entry into the lane's sums (the
 // 4-sample groups outside every lane's range skipped warp-uniformly); q <= 1
 // decides exactly, as in accumulate_used_at.  Returns the lane's smallest
 // accumulated q (2 if none).
@@ -911,60 +877,18 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
   return qmn;
 }
 
-// Pass 1 over a screened list: entries no lane can use are skipped
-// warp-uniformly, and a lane sets up only the entries whose mask holds it;
-// the sums go to `sums` (SmemSums or RegSums).
-// (Taking the used entries two at a time, so their loads and radiance
-// evaluations interleave, measured slower: C3 37.4 vs 34.2 ms, C2 19.6 vs
-// 14.5 on one box -- the pair's second radiance is often wasted and the
-// loop body doubles.)
-// COMPACT (logged forward): the entries some lane used -- the only ones the
-// logged backward needs -- are also written, in list order, over the
-// already-consumed front of sm.mask (read back as int32), and the lanes that
-// used them to sm.umask; returns their count.  sm.list stays whole for the
-// exact emptiness test.
-template <int CH, bool COMPACT = false, class YT, class Sums>
-__device__ inline int accumulate_screened(const SceneView& sv, const RayCtx& r, WarpSmemL& sm,
-                                          int count, bool want, int mc, const SegBase& base,
-                                          float dtf, YT Y, Sums& sums, bool& inside) {
-  int kept = 0;
-  const unsigned lane = threadIdx.x & 31;
-  float qmn = 2.f;
-  for (int i = 0; i < count; ++i) {
-    const unsigned m = sm.mask[i];
-    if (m == 0u) continue;
-    const int64_t p = sm.list[i];
-    const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
-    const unsigned um = __ballot_sync(FULL, u.use);
-    if (!um) continue;
-    if (COMPACT) {
-      if (lane == 0) {
-        sm.mask[kept] = (uint32_t)p;  // kept <= i: masks ahead are intact
-        sm.umask[kept] = um;
-      }
-      ++kept;
-    }
-    float c[3] = {0.f, 0.f, 0.f};
-    if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
-    qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
-  }
-  inside = inside || qmn <= 0.998f;
-  if (COMPACT) __syncwarp();
-  return COMPACT ? kept : count;
-}
-
-// Screen + pass 1 in batches of 32 list entries without a mask array: lane
-// e screens entry b + e and keeps its mask in a register; the batch's
-// screened-in entries are then processed in list order with the mask and
-// the primitive broadcast by shuffles.  Same entries, same order, same
-// arithmetic as screen_list + accumulate_screened, 1 KB less shared memory
-// per warp (more L1 for the register-sum variant, more warps for the
-// shared-memory one).
-template <int CH, class YT, class Sums>
+// Screen + pass 1 in batches of 32 list entries: lane e screens entry b + e
+// and keeps its mask in a register; the batch's screened-in entries are then
+// processed in list order with the mask and the primitive broadcast by
+// shuffles (entries no lane can use are skipped warp-uniformly, and a lane
+// sets up only the entries whose mask holds it).  After each batch every
+// lane calls post(p, lanes that used p) for its entry (0: unused or beyond
+// the list; warp-converged: the logged forward compacts them with a ballot).
+template <int CH, class YT, class Sums, class Post>
 __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, const RayCtx& r,
                                          const WarpSmem& sm, int count, unsigned lanes,
                                          bool want, int mc, const SegBase& base, float dtf, YT Y,
-                                         Sums& sums, bool& inside) {
+                                         Sums& sums, bool& inside, Post&& post) {
   const unsigned lane = threadIdx.x & 31;
   float qmn = 2.f;
   for (int b = 0; b < count; b += 32) {
@@ -972,17 +896,21 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
     const int32_t pl = i < count ? sm.list[i] : 0;
     const unsigned ml = i < count ? screen_entry(sc, pl) & lanes : 0u;
     unsigned todo = __ballot_sync(FULL, ml != 0u);
+    unsigned mine = 0u;  // lanes that used this lane's entry
     while (todo) {
       const int e = __ffs(todo) - 1;
       todo &= todo - 1;
       const unsigned m = __shfl_sync(FULL, ml, e);
       const int64_t p = __shfl_sync(FULL, pl, e);
       const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
-      if (!__any_sync(FULL, u.use)) continue;
+      const unsigned um = __ballot_sync(FULL, u.use);
+      if (lane == (unsigned)e) mine = um;
+      if (!um) continue;
       float c[3] = {0.f, 0.f, 0.f};
       if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
       qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
     }
+    post(pl, mine);
   }
   inside = inside || qmn <= 0.998f;
 }

@@ -47,16 +47,17 @@ while off < head:
     kind = int(h[12:16].view(np.int32)[0])
     mmax = int(h[16:20].view(np.int32)[0])
     act = int(h[20:24].view(np.uint32)[0])
+    cap = int(h[24:28].view(np.int32)[0])
     body = off + 128
     if kind == 1:
-        lst, um = body, body + r16(4 * cnt)
-        size = 128 + r128(r16(4 * cnt) + 4 * cnt)
+        lst, um = body, body + r16(4 * cap)
+        size = 128 + r128(r16(4 * cap) + 4 * cap)
     else:
         nact = bin(act).count("1")
         smp = r16(20 * nact)
         lo = smp + 16 * nact * mmax
-        lst, um = body + lo, body + lo + r16(4 * cnt)
-        size = 128 + r128(lo + r16(4 * cnt) + 4 * cnt)
+        lst, um = body + lo, body + lo + r16(4 * cap)
+        size = 128 + r128(lo + r16(4 * cap) + 4 * cap)
     n_rec[kind] += 1
     m = buf[um:um + 4 * cnt].view(np.uint32).astype(np.int64)
     pc = popc[m & 255] + popc[(m >> 8) & 255] + popc[(m >> 16) & 255] + popc[m >> 24]
