@@ -78,11 +78,13 @@ def workload(name: str):
 
 def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world: int = 1):
     """Training step (fwd + L1/DSSIM loss + bwd + iso loss + Adam, BVH rebuilt
-    every step); target = render of the scene with jittered means.  C2 by
-    default; C4 (3M, 1237x822) with --train-config c4.  Under torchrun every
-    rank renders and back-propagates its interleaved tiles and the [N,87]
-    gradient is NCCL all-reduced (train.Trainer); the step time is the max
-    over ranks."""
+    every step); target = render of the scene with jittered means.  C4 (3M,
+    1237x822: BASELINE configs[3], the train-step metric's config) and C2
+    (300k, 800x800: configs[1]) by default (--train-config).  Under torchrun
+    every rank renders and back-propagates its interleaved tiles, the [N,87]
+    gradient is NCCL reduce-scattered into row shards, each rank runs Adam on
+    its shard and the parameters are all-gathered (train.Trainer); the step
+    time is the max over ranks."""
     import torch
 
     from paper_2509_07782_b200.train import Trainer
@@ -130,7 +132,8 @@ def train_step_bench(G, dev, steps: int, warmup: int, config: str = "c2", world:
            "loss_before": l0, "loss_after": l1, "n_gaussians": int(rec.shape[0]),
            "rays_per_step": cam_kw["width"] * cam_kw["height"], "n_gpus": world}
     if world > 1:  # the phase breakdown below is a single-GPU, full-frame measurement
-        out["parallelism"] = f"tiles{world} + NCCL all-reduce of the [N,87] gradient"
+        out["parallelism"] = (f"tiles{world} + NCCL reduce-scatter of the [N,87] gradient, "
+                              "sharded Adam, all-gather of the parameters")
         return out
     # phase breakdown of one step (device events between the stages)
     from paper_2509_07782_b200.renderer import render, render_backward
@@ -370,7 +373,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true")
-    ap.add_argument("--train-config", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--train-config", default="c4,c2",
+                    help="comma list of c2 / c4: the first is the line's train_step, the "
+                         "others go to train_steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -586,12 +591,19 @@ def main():
             ri.append(1e3 * (time.perf_counter() - t0))
         assert np.array_equal(img, frame[0].double().cpu().numpy())
 
-    train = None
+    train, trains = None, {}
     if not args.no_train:
         del scene
-        torch.cuda.empty_cache()
-        train = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3,
-                                 config=args.train_config, world=world)
+        for i, tc in enumerate(args.train_config.split(",")):
+            if tc not in ("c2", "c4"):
+                raise SystemExit(f"--train-config: unknown config {tc!r}")
+            torch.cuda.empty_cache()
+            res = train_step_bench(G, dev, steps=max(args.steps, 3), warmup=3, config=tc,
+                                   world=world)
+            if i == 0:
+                train = res
+            else:
+                trains[tc] = res
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -646,6 +658,8 @@ def main():
                                           "host buffers allocated there)"}
     if train is not None:
         out["train_step"] = train
+    if trains:
+        out["train_steps"] = trains
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(rec, eps, cam_kw, cfg_kw, target_s=args.cpu_seconds)
         out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
