@@ -770,9 +770,16 @@ __global__ void __launch_bounds__(BWD_THREADS, GSX_BWD_MINB)
 #endif
 template <bool PAIRS>
 struct BwdlShape;
+#ifndef GSX_BWDP_THREADS
+#define GSX_BWDP_THREADS 64
+#endif
+#ifndef GSX_BWDP_MINB
+#define GSX_BWDP_MINB 7
+#endif
 template <>
 struct BwdlShape<true> {
-  static constexpr int threads = 64, minb = 7, warp_floats = PAIR_WARP_FLOATS;
+  static constexpr int threads = GSX_BWDP_THREADS, minb = GSX_BWDP_MINB,
+                       warp_floats = PAIR_WARP_FLOATS;
 };
 template <>
 struct BwdlShape<false> {
