@@ -241,6 +241,9 @@ __device__ inline void log_close(const LogRecPtrs& o, int kept) {
 // kind 0: this lane's per-sample sums (get(j) = (sigma_j, W_j)) of the chunk
 template <class Get>
 __device__ inline void log_samples(const LogRecPtrs& o, int mc, Get&& get) {
+#ifdef GSX_LOG_NO_SAMPLES  // timing experiment only: skip the sample-sum stores
+  return;
+#endif
   if (!o.smp) return;
 #pragma unroll
   for (int j = 0; j < 16; ++j)
