@@ -5,9 +5,11 @@ volume-ratio AABB bound (PAPER.md 1091-1092, geometry.py:193-212).
     python bench_c5.py [--sizes 100000,300000,...] [--aniso 1,10,100,1000]
                        [--width 480 --height 270] [--out profiles/c5_sweep.json]
 
-Per run: the device rebuild (K1 prepare + bounds, K2 Morton, K3 sort, K4
-permute, K5 LBVH + 4-wide collapse) timed with CUDA events (median of 5), the
-forward render of one camera (adaptive + ESS, median of 3) in Mrays/s, and
+Per run: the device rebuild (K1 prepare + bounds, K2 Morton, K3 sort, K5
+LBVH + 4-wide collapse) timed with CUDA events (median of 5; eager launches
+and the CUDA-graph replay), the forward render of one camera (adaptive + ESS,
+median of 3, every forward variant timed and the fastest reported) in
+Mrays/s, and
 per-ray reference-semantics counters on a 4096-ray subset
 (gsx_render_rays_stats): node visits, AABB hits, ellipsoid hits and the
 false-positive fraction (bench.py:181-198).  Scenes: synth_records("ball")
@@ -41,26 +43,28 @@ def run_one(G, n, aniso, bound, width, height, seed=0):
     scene = G.Scene.from_records(rec)
     G.reorder_by_morton(scene)
     s = torch.cuda.current_stream()
-    builds = []
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        scene.rebuild_async()
-        e1.record(s)
-        torch.cuda.synchronize()
-        builds.append(e0.elapsed_time(e1))
+
+    def timed(fn, reps):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    build_ms = timed(scene.rebuild_async, 5)
+    build_graph_ms = timed(scene.rebuild_graphed, 5)
     cam = G.orbit_cameras(1, radius=3.5, focal=1.2 * width, width=width, height=height)[0]
     cfg = G.RenderConfig(mode="adaptive")
-    G.render(scene, cam, cfg)
-    times = []
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        G.render(scene, cam, cfg)
-        e1.record(s)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = float(np.median(times))
+    from paper_2509_07782_b200.renderer import VARIANTS
+
+    by_variant = {v: timed(lambda: G.render(scene, cam, cfg, variant=v), 3) for v in VARIANTS}
+    best = min(by_variant, key=by_variant.get)
+    ms = by_variant[best]
     # reference-semantics counters on a strided ray subset
     step = max(1, int(np.sqrt(width * height / 4096)))
     py, px = np.mgrid[0:height:step, 0:width:step]
@@ -70,8 +74,10 @@ def run_one(G, n, aniso, bound, width, height, seed=0):
     aabb, ell = per[:, 6].sum(), per[:, 7].sum()
     a_eff = min(aniso, 4.914) if bound else aniso
     return {"n": n, "anisotropy": aniso, "bound": bound, "anisotropy_effective": a_eff,
-            "gen_s": round(gen_s, 3), "build_ms": float(np.median(builds)),
-            "render_ms": ms, "mrays_s": width * height / ms / 1e3,
+            "gen_s": round(gen_s, 3), "build_ms": build_ms, "build_graph_ms": build_graph_ms,
+            "render_ms": ms, "render_variant": best,
+            "render_ms_by_variant": {k: round(v, 3) for k, v in by_variant.items()},
+            "mrays_s": width * height / ms / 1e3,
             "node_visits_per_ray": float(per[hit, 5].mean()) if hit.any() else 0.0,
             "aabb_hits_per_ray": float(per[hit, 6].mean()) if hit.any() else 0.0,
             "ellipsoid_hits_per_ray": float(per[hit, 7].mean()) if hit.any() else 0.0,
