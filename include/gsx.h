@@ -36,7 +36,7 @@ extern "C" {
 #endif
 
 #define GSX_FLOATS_PER_RECORD 87
-#define GSX_ABI_VERSION 2
+#define GSX_ABI_VERSION 3
 
 typedef enum {
   GSX_OK = 0,
@@ -70,6 +70,10 @@ typedef struct {
      (32 warps / SM).  Pixels do not depend on it; which is faster depends on
      the device's memory latency (renderer.autotune picks per workload). */
   int64_t sums;
+  /* extension: pass 2 of gsx_render_backward_logged, 0 = by the log's mean
+     lanes per entry, 1 = compacted (lane, primitive) pairs, 2 = all lanes per
+     entry.  Gradients agree to fp32 summation order. */
+  int64_t pass2;
 } gsx_render_cfg;
 
 /* Camera (renderer.py:109-145): camera-to-world rotation R (row-major, from the

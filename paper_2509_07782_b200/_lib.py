@@ -39,7 +39,7 @@ class RenderCfg(ctypes.Structure):
         ("mode", ctypes.c_int64), ("beta", ctypes.c_double), ("dt_min", ctypes.c_double),
         ("dt_max", ctypes.c_double), ("ess", ctypes.c_int64), ("tile_size", ctypes.c_int64),
         ("background", ctypes.c_double * 3), ("buffer_capacity", ctypes.c_int64),
-        ("traversal", ctypes.c_int64), ("sums", ctypes.c_int64),
+        ("traversal", ctypes.c_int64), ("sums", ctypes.c_int64), ("pass2", ctypes.c_int64),
     ]
 
 

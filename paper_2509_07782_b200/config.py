@@ -40,14 +40,16 @@ class RenderConfig:
         if self.mode not in ("uniform", "adaptive"):
             raise ValueError(f"unknown mode {self.mode!r}")
 
-    def to_c(self, traversal: int = 0, sums: int = 0) -> RenderCfg:
-        """C mirror (include/gsx.h gsx_render_cfg); `traversal` and `sums` are
-        the extension fields (traversal: 0 by focal length, 1 packet cone,
-        2 per-lane; sums of the screened forward: 0 shared memory, 1
-        registers)."""
+    def to_c(self, traversal: int = 0, sums: int = 0, pass2: int = 0) -> RenderCfg:
+        """C mirror (include/gsx.h gsx_render_cfg); `traversal`, `sums` and
+        `pass2` are the extension fields (traversal: 0 by focal length, 1
+        packet cone, 2 per-lane; sums of the screened forward: 0 shared memory,
+        1 registers; pass 2 of the logged backward: 0 auto, 1 pairs, 2 all
+        lanes per entry)."""
         c = RenderCfg()
         c.traversal = int(traversal)
         c.sums = int(sums)
+        c.pass2 = int(pass2)
         c.dt, c.n_s, c.t_eps = float(self.dt), int(self.n_s), float(self.t_eps)
         c.mode = 1 if self.mode == "adaptive" else 0
         c.beta, c.dt_min, c.dt_max = float(self.beta), float(self.dt_min), float(self.dt_max)

@@ -675,7 +675,8 @@ int gsx_validate_cfg(const gsx_render_cfg* cfg) {
   if (cfg->dt_min > cfg->dt_max) return GSX_ERR_ARG;
   if (cfg->mode != 0 && cfg->mode != 1) return GSX_ERR_ARG;
   if (!(cfg->dt > 0.0)) return GSX_ERR_ARG;
-  if (cfg->traversal < 0 || cfg->traversal > 2 || cfg->sums < 0 || cfg->sums > 1)
+  if (cfg->traversal < 0 || cfg->traversal > 2 || cfg->sums < 0 || cfg->sums > 1 ||
+      cfg->pass2 < 0 || cfg->pass2 > 2)
     return GSX_ERR_ARG;
   return GSX_OK;
 }

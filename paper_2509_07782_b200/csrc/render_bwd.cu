@@ -785,7 +785,8 @@ template <>
 struct BwdlShape<false> {
   static constexpr int threads = 128, minb = 4, warp_floats = BWD_WARP_FLOATS;
 };
-__device__ inline bool log_wants_pairs(const char* log) {
+__device__ inline bool log_wants_pairs(const char* log, const gsx_render_cfg& cfg) {
+  if (cfg.pass2 != 0) return cfg.pass2 == 1;
   const LogHeader* h = (const LogHeader*)log;
   return 16ull * h->pairs < (unsigned long long)GSX_BWDL_PAIR_MAX * h->entries;
 }
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
                              long long nw, float* __restrict__ grad) {
   constexpr int NT = BwdlShape<PAIRS>::threads, PER_TILE = 256 / NT;
   extern __shared__ __align__(16) float red_smem[];  // BwdlShape::warp_floats per warp
-  if (log_wants_pairs(log) != PAIRS) return;  // the other strategy's launch runs
+  if (log_wants_pairs(log, cfg) != PAIRS) return;  // the other strategy's launch runs
   const long long wid = tile_warp_id(PER_TILE, NT);
   if (!log_complete((void*)log, nw)[wid]) return;  // the replay kernel covers this warp
   const int lane = threadIdx.x & 31;

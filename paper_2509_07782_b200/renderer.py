@@ -177,19 +177,23 @@ def render(scene, camera: Camera, cfg: RenderConfig | None = None, *, tile_begin
 
 def render_backward(scene, camera: Camera, cfg: RenderConfig, rgb, depth, trans, dL_drgb,
                     dL_ddepth=None, dL_dtrans=None, *, grad=None, tile_begin: int = 0,
-                    tile_stride: int = 1, log: MarchLog | None = None, stream=None):
+                    tile_stride: int = 1, log: MarchLog | None = None, stream=None,
+                    pass2: int = 0):
     """Backward of `render` (no reference counterpart):
     accumulates dL/d(records) into grad [N,87] float32 (record layout, storage
     order; allocated zeroed unless given).  rgb/depth/trans are the forward
     outputs of the same tiles; dL_d* are the upstream gradients (CUDA tensors).
-    `log` = the MarchLog the forward of these outputs wrote (skips the replay)."""
+    `log` = the MarchLog the forward of these outputs wrote (skips the replay);
+    `pass2` forces its pass-2 strategy (0 auto from the log, 1 compacted
+    (lane, primitive) pairs, 2 all lanes per entry; same gradients to fp32
+    summation order)."""
     import ctypes
 
     cfg = cfg or RenderConfig()
     L = _lib.lib()
     if grad is None:
         grad = torch.zeros((scene.n, 87), dtype=torch.float32, device=scene.device)
-    cam_c, cfg_c = camera.to_c(), cfg.to_c()
+    cam_c, cfg_c = camera.to_c(), cfg.to_c(pass2=pass2)
     c = lambda t: None if t is None else t.contiguous()  # noqa: E731
     if log is not None:
         if (log.tile_begin, log.tile_stride) != (int(tile_begin), int(tile_stride)):

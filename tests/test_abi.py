@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     for f in funcs:
         assert hasattr(L, f), f
     assert sorted(_lib.EXPORTED) == funcs
-    assert L.gsx_abi_version() == 2
+    assert L.gsx_abi_version() == 3
     assert L.gsx_status_string(0) == b"ok"
     assert L.gsx_scene_arena_bytes(1000) > 1000 * 87 * 4
     assert L.gsx_sort_workspace_bytes(1 << 20) > 0

@@ -41,7 +41,7 @@ def _march_log(G, scene, cam, cfg, log):
     return G.MarchLog(cam, capacity=cap)
 
 
-def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None):
+def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None, pass2=0):
     import torch
 
     scene = G.Scene.from_records(rec, sigma_eps=eps)
@@ -56,7 +56,8 @@ def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None):
     gD = 0.1 * rng.normal(size=(H, W)) if with_depth else np.zeros((H, W))
     gT = rng.normal(size=(H, W))
     t = lambda a: torch.as_tensor(a, dtype=torch.float32, device="cuda")  # noqa: E731
-    grad = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg)
+    grad = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg,
+                             pass2=pass2)
     osc = O.OracleScene(rec, eps)
     rays = O.camera_rays(cam.center, cam.quat, cam.focal, W, H)
     R, T, D, gref = osc.backward_rays(rays, O.OCfg.make(**cfg_kw), gC.reshape(-1, 3),
@@ -97,25 +98,30 @@ def test_backward_c1_adaptive():
     _compare(g, gref)
 
 
+@pytest.mark.parametrize("pass2", [0, 1, 2])
 @pytest.mark.parametrize("log", ["full", "tiny", "partial"])
 @pytest.mark.parametrize("mode", ["uniform", "adaptive"])
-def test_backward_march_log(mode, log):
+def test_backward_march_log(mode, log, pass2):
     """Logged forward + logged backward (march_log.cuh), including arenas too
-    small for some / all warps (those warps fall back to the replay kernel)."""
+    small for some / all warps (those warps fall back to the replay kernel),
+    with pass 2 chosen from the log (0), over compacted pairs (1) and over
+    all lanes per entry (2)."""
     import paper_2509_07782_b200 as G
 
     rec = f32_records(gen_test_scene_records("random-cloud", count=300, seed=4, anisotropy=3.0,
                                              base_scale=0.05))
     cam = G.orbit_cameras(2, radius=3.0, focal=40.0, width=40, height=24)[1]
-    g, gref = _run(G, rec, 0.01, cam, dict(mode=mode, background=(0.2, 0.5, 0.9)), log=log)
+    g, gref = _run(G, rec, 0.01, cam, dict(mode=mode, background=(0.2, 0.5, 0.9)), log=log,
+                   pass2=pass2)
     _compare(g, gref)
 
 
-def test_backward_march_log_c1():
+@pytest.mark.parametrize("pass2", [1, 2])
+def test_backward_march_log_c1(pass2):
     import paper_2509_07782_b200 as G
 
     rec = f32_records(gen_test_scene_records("random-cloud", 10_000, seed=0, anisotropy=3.0,
                                              base_scale=0.01177))
     cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=32, height=32)[0]
-    g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive"), log="full")
+    g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive"), log="full", pass2=pass2)
     _compare(g, gref)
