@@ -377,6 +377,8 @@ def main():
                     help="comma list of c2 / c4: the first is the line's train_step, the "
                          "others go to train_steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--variant", default=None, choices=["screened", "screened-regs", "plain"],
+                    help="force the timed forward kernel (profiling runs; default: autotune)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -487,13 +489,16 @@ def main():
     from paper_2509_07782_b200.renderer import VARIANTS, autotune
 
     tuned = autotune(scene, cam, cfg, tile_begin=tb, tile_stride=ts)
+    if args.variant:  # profiling runs: ncu's serialized replays would mislead the autotune
+        tuned["best"] = args.variant
+        tuned["forced"] = True
     if world > 1:  # every rank runs the same kernel (rank 0's choice)
         choice = torch.tensor([list(VARIANTS).index(tuned["best"])], device=dev)
         dist.broadcast(choice, 0)
         tuned["best"] = list(VARIANTS)[int(choice.item())]
-        from paper_2509_07782_b200 import renderer as _r
+    from paper_2509_07782_b200 import renderer as _r
 
-        _r._TUNED[_r._tune_key(scene, cam, cfg, False, ts)] = tuned["best"]
+    _r._TUNED[_r._tune_key(scene, cam, cfg, False, ts)] = tuned["best"]
     with ClockSampler(local_rank) as clk:
         for _ in range(args.warmup):
             step()
