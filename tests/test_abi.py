@@ -48,6 +48,13 @@ def test_size_queries_and_argument_errors_without_gpu():
     rc = L.gsx_render_forward(None, None, 10, ctypes.byref(cam), ctypes.byref(cfg), 0, 1, None,
                               None, None, None, None, 0, None, None)
     assert rc == _lib.GSX_ERR_ARG  # t_eps must be in (0, 1)
+    cfg.t_eps = 1e-4
+    for field, bad in (("traversal", 3), ("sums", 2), ("pass2", 3), ("pass2", -1)):
+        setattr(cfg, field, bad)
+        rc = L.gsx_render_forward(None, None, 10, ctypes.byref(cam), ctypes.byref(cfg), 0, 1,
+                                  None, None, None, None, None, 0, None, None)
+        assert rc == _lib.GSX_ERR_ARG, field  # extension fields are range-checked
+        setattr(cfg, field, 0)
     assert L.gsx_image_loss(None, None, 8, 8, 3, 0.2, None, None, None, None) == _lib.GSX_ERR_ARG
 
 
