@@ -235,8 +235,6 @@ __device__ inline void box_slab64_f(const float4 lo, const float4 hi, const doub
   box_slab64(l, h, o, d, inv, ta, tb);
 }
 
-__device__ inline int32_t f_as_i(float f) { return __float_as_int(f); }
-
 #define CUDA_CHECK_RET(expr)                       \
   do {                                             \
     cudaError_t _e = (expr);                       \

@@ -380,47 +380,6 @@ __device__ inline void warp_traverse_cone(const BvhView& bv, ConeTrav& st, WarpS
   st.done = st.sp == 0;
 }
 
-// Visit every candidate of the warp's union traversal: f(p) is called by all
-// 32 lanes in lockstep for each staged primitive p (list chunks of LCAP).
-template <class F>
-__device__ inline void for_each_candidate(const BvhView& bv, const RayCtx& r, bool want,
-                                          float lo_t, float hi_t, float gap, WarpSmem& sm,
-                                          uint32_t& visits, F&& f) {
-  WarpTrav st{0, 0, false, false};
-  int count = 0;
-  for (;;) {
-    PH_BEGIN(ph_t)
-    warp_traverse(bv, r, want, lo_t, hi_t, gap, st, sm, count, visits);
-    PH_END(1, ph_t)
-    PH_BEGIN(ph_p)
-    for (int i = 0; i < count; ++i) f((int64_t)sm.list[i]);
-    PH_END(2, ph_p)
-    __syncwarp();
-    count = 0;
-    if (st.done) break;
-  }
-}
-
-// Same traversal, but f(count) is called once per staged chunk of the list.
-template <class F>
-__device__ inline void for_each_chunk(const BvhView& bv, const RayCtx& r, bool want, float lo_t,
-                                      float hi_t, float gap, WarpSmem& sm, uint32_t& visits,
-                                      F&& f) {
-  WarpTrav st{0, 0, false, false};
-  int count = 0;
-  for (;;) {
-    PH_BEGIN(ph_t)
-    warp_traverse(bv, r, want, lo_t, hi_t, gap, st, sm, count, visits);
-    PH_END(1, ph_t)
-    PH_BEGIN(ph_p)
-    f(count);
-    PH_END(2, ph_p)
-    __syncwarp();
-    count = 0;
-    if (st.done) break;
-  }
-}
-
 // Warp-cooperative ESS closest hit (closest_hit spatial.py:309-354): the
 // lanes with `want` find their first ellipsoid entry in [t_lo, t_hi].  One
 // packet traversal of the 4-wide BVH serves all of them (node loads and loop
