@@ -41,10 +41,16 @@ struct PixelGrad {
 //   A (37 rows): 0-9 geometry moments, 10-36 SH (b, c) -> record 11 + 3b + c
 //   B (49 rows): lobe l at 7l: raw axis sum (3), sharpness, amplitude (3)
 // Geometry enters only through the moment tensors of the lane offsets
-// v = x0 - mu (x0 = the lane's sample base point) and the direction d:
+// v = xc - mu and the direction d, with xc the ray's point of closest
+// approach to the primitive (t_c of the setup) and the moments taken in
+// t - t_c:
 //   S0 = m0,  S1 = v m0 + d m1,  S2 = v v^T m0 + (v d^T + d v^T) m1 + d d^T m2
 // (6 unique entries), because with y = M v and u = sqrt(k) y every geometry
-// gradient is linear in them (M = iso_inv, header formulas):
+// gradient is linear in them (M = iso_inv, header formulas).  Centring on
+// t_c keeps |u| <= 1 for every contributing sample: moments about the chunk
+// base (|u0| up to ~40 for a small primitive far into a long adaptive chunk)
+// cancel in u0^2 m0 + 2 u0 ud m1 + ud^2 m2 and cost the scale gradients
+// ~1e-4 of their maximum in fp32 (C4; profiles/r06_grad_err_c4*.json):
 //   dL/dmu = k M^T M S1,  dL/ds_b = k (M S2 M^T)_bb / s_b (unclamped),
 //   dL/dR[a,b] = -sqrt(k) (M S2)_ba / s_b,  dL/dsigma~ = S0 / sigma~,
 // and the SG axis gradient is (I - n n^T)/|a| applied to sum_lanes f d.
@@ -240,10 +246,9 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
       if (use && q <= 1.0f) {
         float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
         float G = fmaf(wos[j], gcl, hh[j]) * dens;
-        float t = (float)j * dtf;
-        m0 += G;
-        m1 = fmaf(G, t, m1);
-        m2 = fmaf(G * t, t, m2);
+        m0 += G;  // moments in del = t_j - t_c (see vc below)
+        m1 = fmaf(G, del, m1);
+        m2 = fmaf(G * del, del, m2);
         e0 = fmaf(wos[j], dens, e0);
       }
     }
@@ -251,9 +256,11 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
   // lanes that do not see p have zero moments: every value below is 0
   {
     const float4 g0 = __ldg(sv.geo + 4 * p);
-    const float v0[3] = {(base.hi[0] - g0.x) + base.lo[0], (base.hi[1] - g0.y) + base.lo[1],
-                         (base.hi[2] - g0.z) + base.lo[2]};
     const float* d = r.df;
+    const float tcu = use ? cs.tc : 0.f;
+    const float v0[3] = {fmaf(d[0], tcu, (base.hi[0] - g0.x) + base.lo[0]),
+                         fmaf(d[1], tcu, (base.hi[1] - g0.y) + base.lo[1]),
+                         fmaf(d[2], tcu, (base.hi[2] - g0.z) + base.lo[2])};
     col[0] = m0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) col[(1 + a) * RED_ROW] = fmaf(v0[a], m0, d[a] * m1);
@@ -570,10 +577,9 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
             const float dens = ex2_approx(fmaf(nkl2, q, cs.lsig));
             const float w = wo[32 * j];
             const float G = fmaf(w, gcl, hp[32 * j]) * dens;
-            const float t = (float)j * dtf;
-            m0 += G;
-            m1 = fmaf(G, t, m1);
-            m2 = fmaf(G * t, t, m2);
+            m0 += G;  // moments in del = t_j - t_c (see grad_candidate)
+            m1 = fmaf(G, del, m1);
+            m2 = fmaf(G * del, del, m2);
             e0 = fmaf(w, dens, e0);
           }
         }
@@ -588,9 +594,11 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
       // ---- P1: geometry moments + SH 0-21
       {
         const float4 g0 = __ldg(sv.geo + 4 * p);
-        const float v0[3] = {(base.hi[0] - g0.x) + base.lo[0], (base.hi[1] - g0.y) + base.lo[1],
-                             (base.hi[2] - g0.z) + base.lo[2]};
         const float* d = rr.df;
+        const float tcu = use ? cs.tc : 0.f;
+        const float v0[3] = {fmaf(d[0], tcu, (base.hi[0] - g0.x) + base.lo[0]),
+                             fmaf(d[1], tcu, (base.hi[1] - g0.y) + base.lo[1]),
+                             fmaf(d[2], tcu, (base.hi[2] - g0.z) + base.lo[2])};
         col[0] = m0;
 #pragma unroll
         for (int a = 0; a < 3; ++a) col[(1 + a) * PR_ROW] = fmaf(v0[a], m0, d[a] * m1);

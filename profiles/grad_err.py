@@ -1,9 +1,9 @@
-"""Error structure of the C2 backward (sparse pixel mask) against the
-float64 oracle backward: per parameter group, the relative error of the
+"""Error structure of the C2 (or C4) backward (sparse pixel mask) against
+the float64 oracle backward: per parameter group, the relative error of the
 entries by magnitude bin (|g| / max|g| of the group), for the replay and
-the logged backward.
+the logged backward (both pass-2 strategies).
 
-    python profiles/grad_err.py > gpurun_out/grad_err.json
+    python profiles/grad_err.py [c2|c4] > gpurun_out/grad_err.json
 """
 import json
 import os
@@ -18,9 +18,10 @@ import torch  # noqa: E402
 import oracle as O  # noqa: E402
 from test_gpu_bench_parity import _pixels, _setup  # noqa: E402
 
-G, rec, eps, scene, cam, cfg, cfg_kw = _setup("c2")
+CFG = sys.argv[1] if len(sys.argv) > 1 else "c2"
+G, rec, eps, scene, cam, cfg, cfg_kw = _setup(CFG)
 H, W = cam.height, cam.width
-rays, py, px = _pixels(cam, 40, 17, 23)
+rays, py, px = _pixels(cam, *((40, 17, 23) if CFG == "c2" else (64, 21, 29)))
 rng = np.random.default_rng(3)
 gC = np.zeros((H, W, 3)); gT = np.zeros((H, W)); gD = np.zeros((H, W))
 gC[py, px] = rng.normal(size=(len(py), 3))
@@ -32,7 +33,7 @@ _, _, _, g_ref = osc.backward_rays(rays, O.OCfg.make(**cfg_kw), gC[py, px], gD[p
                                    gT[py, px], clip=True)
 uids = scene.uids
 res = {}
-for log in (None, "full"):
+for log, pass2 in ((None, 0), ("full", 1), ("full", 2)):
     lg = None
     if log:
         lg = G.MarchLog(cam)
@@ -41,7 +42,8 @@ for log in (None, "full"):
             if not lg.ensure():
                 break
     rgb, depth, trans, _ = G.render(scene, cam, cfg, log=lg)
-    g = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg)
+    g = G.render_backward(scene, cam, cfg, rgb, depth, trans, t(gC), t(gD), t(gT), log=lg,
+                          pass2=pass2)
     g_gpu = np.empty_like(g_ref)
     g_gpu[uids] = g.cpu().numpy()
     out = {}
@@ -60,5 +62,5 @@ for log in (None, "full"):
                                           "rel_p99": float(np.quantile(rel[m], 0.99)),
                                           "abs_over_gmax_max": float(absn[m].max())}
         out[name] = {"gmax": float(gmax), "abs_over_gmax_max": float(absn.max()), "bins": bins}
-    res[str(log)] = out
+    res[f"{log}/pass2={pass2}"] = out
 print(json.dumps(res, indent=1))

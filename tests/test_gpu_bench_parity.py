@@ -11,8 +11,9 @@ oracle on stratified pixel subsets.
   zero, in the same summation order, so the screened frame equals the
   unscreened one to fp32 contraction noise (bitwise on the r06 build; a
   wrongly screened-out pair would show far above the 2e-6 bound).
-* C2 (300k, 800x800, uniform + ESS, white background) backward: dL/dI is
-  non-zero only on a sparse pixel mask, so the oracle's analytic float64
+* C2 (300k, 800x800, uniform + ESS, white background) and C4 (3M,
+  1237x822, adaptive + ESS) backward: dL/dI is non-zero only on a sparse
+  pixel mask, so the oracle's analytic float64
   backward (oracle/gsray_oracle.c, FD-pinned in test_oracle_grad.py) is
   affordable at full scene size.  Element-wise: every gradient entry with
   |g| >= 1e-2 max|g| of its parameter group agrees to relative 1e-3, and
@@ -94,12 +95,15 @@ def test_c4_frame_vs_oracle():
     assert _forward_subset("c4", 32, 5, 13) == 26 * 39
 
 
-def test_c2_backward_sparse_mask_vs_oracle():
+def _backward_sparse(name, stride, oy, ox, runs):
+    """Backward of config `name` with dL/dI on every `stride`-th pixel per
+    axis vs the oracle's analytic backward, element-wise (module docstring);
+    runs = ((march log?, pass2), ...)."""
     import torch
 
-    G, rec, eps, scene, cam, cfg, cfg_kw = _setup("c2")
+    G, rec, eps, scene, cam, cfg, cfg_kw = _setup(name)
     H, W = cam.height, cam.width
-    rays, py, px = _pixels(cam, 40, 17, 23)  # 20 x 20 = 400 pixels
+    rays, py, px = _pixels(cam, stride, oy, ox)
     rng = np.random.default_rng(3)
     gC = np.zeros((H, W, 3))
     gT = np.zeros((H, W))
@@ -112,9 +116,7 @@ def test_c2_backward_sparse_mask_vs_oracle():
     _, _, _, g_ref = osc.backward_rays(rays, O.OCfg.make(**cfg_kw), gC[py, px], gD[py, px],
                                        gT[py, px], clip=True)
     uids = scene.uids  # GPU storage position -> original record index
-    # replay backward; logged backward with pass 2 over all lanes per entry
-    # (what C2's 14 lanes per entry selects) and over compacted pairs (C4's)
-    for log, pass2 in ((None, 0), ("full", 2), ("full", 1)):
+    for log, pass2 in runs:
         lg = None
         if log:
             lg = G.MarchLog(cam)
@@ -129,15 +131,29 @@ def test_c2_backward_sparse_mask_vs_oracle():
                               pass2=pass2)
         g_gpu = np.empty_like(g_ref)
         g_gpu[uids] = g.cpu().numpy()
-        for name, (a, b) in {"mean": (0, 3), "quat": (3, 7), "scale": (7, 10),
-                             "sigma": (10, 11), "sh": (11, 38), "axis": (38, 59),
-                             "sharp": (59, 66), "amp": (66, 87)}.items():
+        for gname, (a, b) in {"mean": (0, 3), "quat": (3, 7), "scale": (7, 10),
+                              "sigma": (10, 11), "sh": (11, 38), "axis": (38, 59),
+                              "sharp": (59, 66), "amp": (66, 87)}.items():
             A, B = g_gpu[:, a:b], g_ref[:, a:b]
             gmax = np.abs(B).max()
-            assert gmax > 0, name
+            assert gmax > 0, gname
             big = np.abs(B) >= 1e-2 * gmax
             rel = np.abs(A - B)[big] / np.abs(B)[big]
-            assert rel.max() <= 1e-3, (log, pass2, name, rel.max(), int(big.sum()))
+            assert rel.max() <= 1e-3, (name, log, pass2, gname, rel.max(), int(big.sum()))
             # every entry: relative 1e-3 above the fp32 floor of 2e-5 max|g|
             err = np.abs(A - B) - 1e-3 * np.abs(B)
-            assert err.max() <= 2e-5 * gmax, (log, pass2, name, err.max(), gmax)
+            assert err.max() <= 2e-5 * gmax, (name, log, pass2, gname, err.max(), gmax)
+
+
+def test_c2_backward_sparse_mask_vs_oracle():
+    # 20 x 20 = 400 pixels; replay backward, logged backward over all lanes
+    # per entry (what C2's 14 lanes per entry selects) and over compacted pairs
+    _backward_sparse("c2", 40, 17, 23, ((None, 0), ("full", 2), ("full", 1)))
+
+
+def test_c4_backward_sparse_mask_vs_oracle():
+    # 3M Gaussians, 1237 x 822, adaptive: every 64th pixel per axis (13 x 20 =
+    # 260 pixels); the logged backward as the trainer runs it (pass 2 chosen
+    # from the log: compacted pairs at C4's 7.7 lanes per entry) and forced to
+    # all lanes per entry
+    _backward_sparse("c4", 64, 21, 29, (("full", 0), ("full", 2)))
