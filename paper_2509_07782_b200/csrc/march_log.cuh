@@ -51,7 +51,8 @@ struct LogRec {
   int mmax;        // samples stored per active lane (warp max of mc), kind 0
   unsigned act;    // lanes stored (mc > 0), kind 0
   int cap;         // entries the list / umask arrays were sized for (>= count)
-  int pad[25];
+  int swidth;      // sample-sum array: 0 = nact columns by slot, 32 = all lanes by lane
+  int pad[24];
 };
 static_assert(sizeof(LogRec) == 128, "LogRec is one 128-byte line");
 
@@ -61,11 +62,13 @@ __host__ __device__ inline long long log_round16(long long x) { return (x + 15) 
 // byte offsets inside a kind-0 body for nact stored lanes
 struct LogLayout {
   long long dt, mc, smp, list, umask, bytes;
-  __host__ __device__ LogLayout(int nact, int mmax, int count) {
+  // sw: columns of the sample-sum array (nact, or 32 when stored by lane)
+  __host__ __device__ LogLayout(int nact, int mmax, int count, int sw = -1) {
+    if (sw < 0) sw = nact;
     dt = 8LL * nact;
     mc = 16LL * nact;
     smp = log_round16(20LL * nact);
-    list = smp + 16LL * nact * mmax;
+    list = smp + 16LL * sw * mmax;
     umask = list + log_round16(4LL * count);
     bytes = 128 + log_round128(umask + 4LL * count);
   }
@@ -99,6 +102,7 @@ struct LogWriter {
   long long need;  // bytes this warp's records need, logged or not
   unsigned entries, pairs;  // this lane's share of the logged entries / pairs
   bool on;
+  bool bulk;  // a bulk copy of shared-memory sums may still be reading them
 };
 
 __device__ inline LogWriter log_writer(void* base, long long wid) {
@@ -110,6 +114,7 @@ __device__ inline LogWriter log_writer(void* base, long long wid) {
   w.need = 0;
   w.entries = w.pairs = 0u;
   w.on = base != nullptr;
+  w.bulk = false;
   return w;
 }
 
@@ -147,6 +152,7 @@ __device__ inline void log_header(const LogWriter& w, long long off, int cap, in
     r->next = -1;
     r->count = 0;  // log_close
     r->cap = cap;
+    r->swidth = 0;
     r->kind = kind;
     r->mmax = mmax;
     r->act = act;
@@ -169,15 +175,25 @@ struct LogRecPtrs {
   LogRec* hdr;
   int32_t* list;
   uint32_t* umask;
-  float4* smp;  // this lane's first sample-sum slot (kind 0, lanes with samples)
+  float4* smp;  // this lane's first sample-sum slot (kind 0, lanes with samples);
+                // by-lane records: the array base (warp-uniform)
   int nact, mmax;
+  bool by_lane;
 };
 
 // Warp-uniform.  final: the chunk's last list (kind 0, lane block written
 // here: tb, dt, this lane's sample count mc); else a kind-1 list chunk.
+// by_lane: the sample-sum array gets 32 columns indexed by lane (written in
+// one bulk copy from the shared-memory sums, log_samples_bulk), or -- with
+// GSX_LOG_BULK_MIN > 0 -- only when that many lanes have samples (less
+// padding; C2 logged forward 17.1 ms with 24 vs 16.1 with 0 / always: the
+// kernel then carries both store paths).
+#ifndef GSX_LOG_BULK_MIN
+#define GSX_LOG_BULK_MIN 0
+#endif
 __device__ inline LogRecPtrs log_open(LogWriter& w, int count, bool final, double tb,
-                                      double dt, int mc) {
-  LogRecPtrs o{nullptr, nullptr, nullptr, nullptr, 0, 0};
+                                      double dt, int mc, bool by_lane = false) {
+  LogRecPtrs o{nullptr, nullptr, nullptr, nullptr, 0, 0, false};
   if (!w.base) return o;
   if (!final) {
     const long long off = log_alloc(w, log_chunk_bytes(count));
@@ -193,10 +209,12 @@ __device__ inline LogRecPtrs log_open(LogWriter& w, int count, bool final, doubl
   const unsigned act = __ballot_sync(0xffffffffu, mc > 0);
   const int nact = __popc(act);
   const int mmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)(mc > 0 ? mc : 0));
-  const LogLayout L(nact, mmax, count);
+  by_lane = by_lane && nact >= GSX_LOG_BULK_MIN;
+  const LogLayout L(nact, mmax, count, by_lane ? 32 : nact);
   const long long off = log_alloc(w, L.bytes);
   if (off < 0) return o;
   log_header(w, off, count, 0, mmax, act);
+  if (by_lane && lane == 0) ((LogRec*)(w.base + off))->swidth = 32;
   char* body = w.base + off + 128;
   o.hdr = (LogRec*)(w.base + off);
   o.list = (int32_t*)(body + L.list);
@@ -208,8 +226,10 @@ __device__ inline LogRecPtrs log_open(LogWriter& w, int count, bool final, doubl
     __stcs((double*)body + slot, tb);
     __stcs((double*)(body + L.dt) + slot, dt);
     __stcs((int*)(body + L.mc) + slot, mc);
-    o.smp = (float4*)(body + L.smp) + slot;
+    if (!by_lane) o.smp = (float4*)(body + L.smp) + slot;
   }
+  if (by_lane) o.smp = (float4*)(body + L.smp);
+  o.by_lane = by_lane;
   return o;
 }
 
@@ -219,8 +239,38 @@ __device__ inline LogRecPtrs log_open(LogWriter& w, int count, bool final, doubl
 // warps per issue); the 64-register kernels are faster with it inline
 // (C4 register-sum 28.2 vs 29.4 ms).
 static __device__ __noinline__ LogRecPtrs log_open_ool(LogWriter& w, int count, bool final,
-                                                       double tb, double dt, int mc) {
-  return log_open(w, count, final, tb, dt, mc);
+                                                       double tb, double dt, int mc,
+                                                       bool by_lane) {
+  return log_open(w, count, final, tb, dt, mc, by_lane);
+}
+
+// By-lane records: the chunk's sums, acc[0 .. mmax)[32] float4 in shared
+// memory (WarpSmemA), go to the record in one TMA bulk copy issued by lane 0
+// (cp.async.bulk, completion tracked in a bulk group) instead of 16 vector
+// stores per lane.  The shared source must not be rewritten before
+// log_bulk_wait.  Warp-uniform.
+__device__ inline bool log_samples_bulk(const LogRecPtrs& o, const float4* acc) {
+  if (!o.by_lane || o.mmax == 0) return false;
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned src = (unsigned)__cvta_generic_to_shared(acc);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o.smp),
+                 "r"(src), "r"((unsigned)(o.mmax * 32 * 16))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  return true;
+}
+// the shared sums may be rewritten once the pending bulk copy has read them
+__device__ inline void log_bulk_wait() {
+  if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+}
+// end of the warp: every bulk copy complete (source reads and global writes)
+__device__ inline void log_bulk_drain() {
+  if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
 }
 
 // kept entry k of the open record: primitive p and the lanes um that used it

@@ -130,7 +130,7 @@ __device__ bool forward_segment(const SceneView& sv, const BvhView& bv, const Ra
       if (!STATS && gate && !nonempty && exact_aabb_overlap(sv, r, p, seg.t0, seg.t1))
         nonempty = true;
     };
-    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0};
+    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0, false};
     for (;;) {
       PH_BEGIN(ph_t)
       if (CONE)
@@ -308,6 +308,9 @@ __global__ void __launch_bounds__(NT, GSX_FWD_MINB * FWD_THREADS / NT) k_render_
 // march, same per-lane arithmetic in the same order: its pixels equal the
 // unscreened kernel's bit for bit.
 // ---------------------------------------------------------------------------
+#ifndef GSX_LOG_BULK  // training forward, shared-memory sums: TMA bulk copy of the sums
+#define GSX_LOG_BULK 1
+#endif
 template <bool SAVE, bool SMEM, class YT, class WS>
 __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
                                          const RayCtx& r, bool want, const Seg& seg, int ns,
@@ -328,7 +331,10 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     if (!__any_sync(FULL, wch)) continue;
     const double tb = seg.tbase + (double)(ch * CH) * seg.dt;
     const SegBase base = seg_base(r, tb);
-    sums.zero(CH);
+    // the training forward's shared-memory sums are zeroed after the first
+    // traversal: a bulk copy of the previous chunk's may still be reading them
+    constexpr bool BULK = SAVE && SMEM && GSX_LOG_BULK;
+    if constexpr (!BULK) sums.zero(CH);
     SegLimits lim;
     if (nchunks == 1) {
       lim = seg_limits(r, seg);
@@ -345,12 +351,21 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     const unsigned lanes = __ballot_sync(FULL, wch && mc > 0);
     const bool save = SAVE && __any_sync(FULL, want && mc > 0);
     int count = 0;
-    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0};
+    LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0, false};
+    bool zeroed = false;
     for (;;) {
       warp_traverse_cone(bv, cst, sm, count, visits);
+      if constexpr (BULK) {
+        if (!zeroed) {
+          if (lw.bulk) log_bulk_wait();
+          lw.bulk = false;
+          sums.zero(CH);
+          zeroed = true;
+        }
+      }
       if constexpr (SAVE) {
         if (save)
-          lo = SMEM ? log_open_ool(lw, count, cst.done, tb, seg.dt, mc)
+          lo = SMEM ? log_open_ool(lw, count, cst.done, tb, seg.dt, mc, BULK)
                     : log_open(lw, count, cst.done, tb, seg.dt, mc);
       }
       bool inside = false;
@@ -377,7 +392,15 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       if (cst.done) break;
       count = 0;
     }
-    if constexpr (SAVE) log_samples(lo, mc, [&](int j) { return sums.get(j); });
+    if constexpr (BULK) {
+      if (GSX_LOG_BULK_MIN == 0 || lo.by_lane) {
+        if (log_samples_bulk(lo, &sm.acc[0][0])) lw.bulk = true;
+      } else {
+        log_samples(lo, mc, [&](int j) { return sums.get(j); });
+      }
+    } else if constexpr (SAVE) {
+      log_samples(lo, mc, [&](int j) { return sums.get(j); });
+    }
     // front-to-back compositing (renderer.py:230-239)
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -458,6 +481,7 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
                             return forward_segment_screened<SAVE, SMEM>(sv, bv, r, want, seg,
                                                                         ns, Yv, acc, sw, sc, lw);
                           });
+  if (SAVE && lw.bulk) log_bulk_drain();
   if (SAVE) log_finish(lw, log_nw);
   ovf_report(sw, bv, py * W + px);
   if (valid) {

@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
     const unsigned act = h->act;
     const int mmax = h->mmax;
     const long long next = h->next;
-    const LogLayout Lo(__popc(act), mmax, h->cap);
+    const int sw = h->swidth ? h->swidth : __popc(act);  // sample-sum columns
+    const LogLayout Lo(__popc(act), mmax, h->cap, sw);
     if (next >= 0) log_prefetch(log + next, 128 + Lo.list);
     const bool mine = (act >> lane) & 1u;
     const int slot = __popc(act & ((1u << lane) - 1u));
@@ -846,8 +847,8 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
       dt = __ldcs((const double*)(body + Lo.dt) + slot);
       mc = __ldcs((const int*)(body + Lo.mc) + slot);
     }
-    const float4* smp = (const float4*)(body + Lo.smp) + slot;
-    const int nact = __popc(act);
+    const float4* smp = (const float4*)(body + Lo.smp) + (h->swidth ? lane : slot);
+    const int nact = sw;  // the sample array's row stride
     const float dtf = (float)dt;
     float wos[16], hh[16];
 #if GSX_BWD_LDGRP

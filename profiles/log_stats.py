@@ -48,6 +48,7 @@ while off < head:
     mmax = int(h[16:20].view(np.int32)[0])
     act = int(h[20:24].view(np.uint32)[0])
     cap = int(h[24:28].view(np.int32)[0])
+    sw = int(h[28:32].view(np.int32)[0])
     body = off + 128
     if kind == 1:
         lst, um = body, body + r16(4 * cap)
@@ -55,7 +56,7 @@ while off < head:
     else:
         nact = bin(act).count("1")
         smp = r16(20 * nact)
-        lo = smp + 16 * nact * mmax
+        lo = smp + 16 * (sw or nact) * mmax
         lst, um = body + lo, body + lo + r16(4 * cap)
         size = 128 + r128(lo + r16(4 * cap) + 4 * cap)
     n_rec[kind] += 1
