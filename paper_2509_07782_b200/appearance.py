@@ -10,7 +10,6 @@ like the reference, or many at once through `eval_fields_batch`.
 
 from __future__ import annotations
 
-import ctypes
 import math
 from dataclasses import dataclass
 
