@@ -6,7 +6,6 @@ AABBs).  Closest hits agree to ~1e-12 (fp64 Kahan quadratic)."""
 
 from __future__ import annotations
 
-
 import numpy as np
 import torch
 

@@ -18,7 +18,6 @@ full parameter set and builds its own (deterministic, identical) BVH.
 
 from __future__ import annotations
 
-
 import numpy as np
 import torch
 
