@@ -28,26 +28,26 @@ def _compare(g_gpu, g_ref, tol_l2=1e-3, tol_max=2e-3):
         assert errmax <= tol_max * np.abs(B).max() + floor_max, (g, errmax, np.abs(B).max())
 
 
-def _march_log(G, scene, cam, cfg, log):
+def _march_log(G, scene, cam, cfg, log, variant=None):
     """MarchLog for mode 'full' (fits), 'tiny' (no warp fits: every warp is
     replayed) or 'partial' (some warps fit, the rest are replayed)."""
     if log is None:
         return None
     probe = G.MarchLog(cam, capacity=1 << 28)
-    G.render(scene, cam, cfg, log=probe)
+    G.render(scene, cam, cfg, log=probe, variant=variant)
     used, ovf = probe.usage()
     assert not ovf and used > probe.min_bytes
     cap = {"full": used, "tiny": probe.min_bytes, "partial": (probe.min_bytes + used) // 2}[log]
     return G.MarchLog(cam, capacity=cap)
 
 
-def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None, pass2=0):
+def _run(G, rec, eps, cam, cfg_kw, seed=0, with_depth=True, log=None, pass2=0, variant=None):
     import torch
 
     scene = G.Scene.from_records(rec, sigma_eps=eps)
     cfg = G.RenderConfig(**cfg_kw)
-    lg = _march_log(G, scene, cam, cfg, log)
-    rgb, depth, trans, _ = G.render(scene, cam, cfg, log=lg)
+    lg = _march_log(G, scene, cam, cfg, log, variant)
+    rgb, depth, trans, _ = G.render(scene, cam, cfg, log=lg, variant=variant)
     if lg is not None:
         assert lg.usage()[1] == (log != "full")
     rng = np.random.default_rng(seed)
@@ -114,6 +114,24 @@ def test_backward_march_log(mode, log, pass2):
     g, gref = _run(G, rec, 0.01, cam, dict(mode=mode, background=(0.2, 0.5, 0.9)), log=log,
                    pass2=pass2)
     _compare(g, gref)
+
+
+@pytest.mark.parametrize("variant", ["screened", "screened-regs", "plain"])
+@pytest.mark.parametrize("log", ["full", "partial"])
+def test_backward_march_log_variants(variant, log):
+    """The training forward's three kernels write different record layouts
+    (sample sums by lane via a bulk copy from shared memory, or by active-lane
+    slot from registers); the backward must read each, with both pass-2
+    strategies."""
+    import paper_2509_07782_b200 as G
+
+    rec = f32_records(gen_test_scene_records("random-cloud", count=300, seed=4, anisotropy=3.0,
+                                             base_scale=0.05))
+    cam = G.orbit_cameras(2, radius=3.0, focal=40.0, width=40, height=24)[1]
+    for pass2 in (1, 2):
+        g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive", background=(0.2, 0.5, 0.9)),
+                       log=log, pass2=pass2, variant=variant)
+        _compare(g, gref)
 
 
 @pytest.mark.parametrize("pass2", [1, 2])
