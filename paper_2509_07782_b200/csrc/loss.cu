@@ -230,41 +230,73 @@ __global__ void k_iso_loss(const float* __restrict__ params, int64_t n, double r
 struct AdamArgs {
   const float* lr87;
   const float* lo87;
-  float b1, b2, eps, bc1, bc2;
+  float b1, b2, eps, ibc1, isbc2;  // 1 / (1 - b1^t), 1 / sqrt(1 - b2^t)
 };
-__device__ __forceinline__ float adam_one(float& pi, float gi, float& mi, float& vi, int slot,
-                                          const AdamArgs& a) {
+__device__ __forceinline__ void adam_one(float& pi, float gi, float& mi, float& vi, int slot,
+                                         const AdamArgs& a) {
   mi = fmaf(a.b1, mi, (1.f - a.b1) * gi);
   vi = fmaf(a.b2, vi, (1.f - a.b2) * gi * gi);
-  const float np_ = pi - __ldg(a.lr87 + slot) * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
+  // p -= lr (m / bc1) / (sqrt(v / bc2) + eps): one division
+  const float np_ = pi - __ldg(a.lr87 + slot) * a.ibc1 * mi / fmaf(sqrtf(vi), a.isbc2, a.eps);
   // projection onto the record's validity domain (sigma~ > sigma_eps,
   // scales > 0, sharpness >= 0): lo87 = per-slot lower bound (-inf = none)
   pi = fmaxf(np_, __ldg(a.lo87 + slot));
-  return pi;
 }
+__device__ __forceinline__ int slot_next(int s) { return s + 1 - (s + 1 >= GSX_NREC ? GSX_NREC : 0); }
+__device__ __forceinline__ void adam_f4(float4& pp, const float4& gg, float4& mm, float4& vv,
+                                        int slot, const AdamArgs& a) {
+  const int s1 = slot_next(slot), s2 = slot_next(s1), s3 = slot_next(s2);
+  adam_one(pp.x, gg.x, mm.x, vv.x, slot, a);
+  adam_one(pp.y, gg.y, mm.y, vv.y, s1, a);
+  adam_one(pp.z, gg.z, mm.z, vv.z, s2, a);
+  adam_one(pp.w, gg.w, mm.w, vv.w, s3, a);
+}
+// ILP float4s of each stream in flight per thread and iteration (grid-stride
+// over CTAs sized to the device); the record slot of each is carried.
+// 3M records (profiles/adam_bw.py): one float4 per thread and stream, one
+// CTA per 256 of them: 1.05 ms = 7.0 TB/s of the 28 B/value; grid-stride
+// over 8 / 16 CTAs per SM with 1-4 float4 in flight per thread 1.16-1.20 ms;
+// the two-division form 1.89 ms.
+#ifndef GSX_ADAM_CTAS  // CTAs per SM of the grid-stride loop
+#define GSX_ADAM_CTAS (1 << 20)
+#endif
+#ifndef GSX_ADAM_ILP
+#define GSX_ADAM_ILP 1
+#endif
 __global__ void __launch_bounds__(256) k_adam4(float4* __restrict__ p, const float4* __restrict__ g,
                                                float4* __restrict__ m, float4* __restrict__ v,
                                                int64_t n4, AdamArgs a) {
+  constexpr int ILP = GSX_ADAM_ILP;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n4) return;
-  int slot = (int)((4 * q) % GSX_NREC);
-  const int step = (int)((4 * stride) % GSX_NREC);
-  for (; q < n4; q += stride) {
-    float4 pp = p[q], mm = m[q], vv = v[q];
-    const float4 gg = __ldcs(g + q);
-    const int s1 = slot + 1 - (slot + 1 >= GSX_NREC ? GSX_NREC : 0);
-    const int s2 = s1 + 1 - (s1 + 1 >= GSX_NREC ? GSX_NREC : 0);
-    const int s3 = s2 + 1 - (s2 + 1 >= GSX_NREC ? GSX_NREC : 0);
-    adam_one(pp.x, gg.x, mm.x, vv.x, slot, a);
-    adam_one(pp.y, gg.y, mm.y, vv.y, s1, a);
-    adam_one(pp.z, gg.z, mm.z, vv.z, s2, a);
-    adam_one(pp.w, gg.w, mm.w, vv.w, s3, a);
-    p[q] = pp;
-    m[q] = mm;
-    v[q] = vv;
-    slot += step;
-    slot -= slot >= GSX_NREC ? GSX_NREC : 0;
+  int slot[ILP];
+#pragma unroll
+  for (int u = 0; u < ILP; ++u) slot[u] = (int)((4 * (q + u * stride)) % GSX_NREC);
+  const int step = (int)((4 * ILP * stride) % GSX_NREC);
+  for (; q < n4; q += ILP * stride) {
+    float4 pp[ILP], mm[ILP], vv[ILP], gg[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; ++u) {
+      const int64_t k = q + u * stride;
+      if (k < n4) {
+        pp[u] = p[k];
+        mm[u] = m[k];
+        vv[u] = v[k];
+        gg[u] = __ldcs(g + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; ++u) {
+      const int64_t k = q + u * stride;
+      if (k < n4) {
+        adam_f4(pp[u], gg[u], mm[u], vv[u], slot[u], a);
+        p[k] = pp[u];
+        m[k] = mm[u];
+        v[k] = vv[u];
+      }
+      slot[u] += step;
+      slot[u] -= slot[u] >= GSX_NREC ? GSX_NREC : 0;
+    }
   }
 }
 // scalar tail / unaligned views (a row shard of the padded parameters)
@@ -342,15 +374,19 @@ extern "C" int gsx_adam_step(float* params, const float* grad, float* m, float* 
   if (n <= 0 || step < 1) return GSX_ERR_ARG;
   int64_t count = n * GSX_NREC;
   const AdamArgs a{lr87, lo87, (float)beta1, (float)beta2, (float)eps,
-                   (float)(1.0 - pow(beta1, (double)step)), (float)(1.0 - pow(beta2, (double)step))};
+                   (float)(1.0 / (1.0 - pow(beta1, (double)step))),
+                   (float)(1.0 / sqrt(1.0 - pow(beta2, (double)step)))};
   cudaStream_t s = (cudaStream_t)stream;
   int64_t done = 0;
   if ((((uintptr_t)params | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) == 0) {
     const int64_t n4 = count / 4;
     if (n4 > 0) {
-      // one float4 per thread (a grid-stride loop over 8 CTAs per SM measured
-      // 1.93 vs 1.89 ms for the 3M-record C4 step; ~3.8 TB/s either way)
-      const int64_t blocks = std::min<int64_t>((n4 + 255) / 256, (int64_t)INT32_MAX);
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t blocks =
+          std::min<int64_t>((n4 + 256 * GSX_ADAM_ILP - 1) / (256 * GSX_ADAM_ILP),
+                            (int64_t)sms * GSX_ADAM_CTAS);
       k_adam4<<<(unsigned)blocks, 256, 0, s>>>((float4*)params, (const float4*)grad, (float4*)m,
                                                (float4*)v, n4, a);
       done = 4 * n4;
