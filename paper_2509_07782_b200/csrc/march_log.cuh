@@ -251,10 +251,12 @@ static __device__ __noinline__ LogRecPtrs log_open_ool(LogWriter& w, int count, 
 // log_bulk_wait.  Warp-uniform.
 __device__ inline bool log_samples_bulk(const LogRecPtrs& o, const float4* acc) {
   if (!o.by_lane || o.mmax == 0) return false;
+  // every lane's shared-memory writes made visible to the async proxy, then
+  // one lane issues the copy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
     const unsigned src = (unsigned)__cvta_generic_to_shared(acc);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o.smp),
                  "r"(src), "r"((unsigned)(o.mmax * 32 * 16))
                  : "memory");
