@@ -417,11 +417,20 @@ def main():
 
     import torch
 
+    # GSX_BENCH_FUNCTIONAL=1: a functional check of the N > 1 code path on a
+    # box with fewer GPUs (every rank on cuda:0, gloo collectives); its
+    # timings mean nothing
+    functional = os.environ.get("GSX_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_2509_07782_b200 as G
     from paper_2509_07782_b200 import _lib
     from paper_2509_07782_b200.train import gather_tiles
