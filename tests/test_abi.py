@@ -99,3 +99,41 @@ def test_camera_rays_vectorised_matches_ray():
         one = cam.ray(px, py)
         np.testing.assert_array_equal(r[py * 9 + px, 0:3], one.origin)
         np.testing.assert_allclose(r[py * 9 + px, 3:6], one.direction, rtol=0, atol=1e-15)
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors in _lib.py have the size and field offsets of the
+    C structs in include/gsx.h (compiled here with gcc)."""
+    import shutil
+    import subprocess
+
+    from paper_2509_07782_b200 import _lib
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = Path(__file__).resolve().parent.parent
+    checks = {
+        "gsx_render_cfg": (_lib.RenderCfg, ["dt", "n_s", "t_eps", "mode", "background",
+                                             "buffer_capacity", "traversal", "sums", "pass2"]),
+        "gsx_camera": (_lib.CameraC, [f for f, _ in _lib.CameraC._fields_]),
+        "gsx_stats": (_lib.Stats, ["rays", "composited"]),
+    }
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "gsx.h"', "int main(void) {"]
+    for st, (_, fields) in checks.items():
+        lines.append(f'  printf("{st} size %zu\\n", sizeof({st}));')
+        for f in fields:
+            lines.append(f'  printf("{st} {f} %zu\\n", offsetof({st}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(root / "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    got = {}
+    for line in out.splitlines():
+        st, key, val = line.split()
+        got[(st, key)] = int(val)
+    for st, (cls, fields) in checks.items():
+        assert got[(st, "size")] == ctypes.sizeof(cls), st
+        for f in fields:
+            assert got[(st, f)] == getattr(cls, f).offset, (st, f)
