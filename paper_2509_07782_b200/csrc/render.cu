@@ -354,7 +354,9 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
     LogRecPtrs lo{nullptr, nullptr, nullptr, nullptr, 0, 0, false};
     bool zeroed = false;
     for (;;) {
+      PH_BEGIN(ph_t)
       warp_traverse_cone(bv, cst, sm, count, visits);
+      PH_END(1, ph_t)
       if constexpr (BULK) {
         if (!zeroed) {
           if (lw.bulk) log_bulk_wait();
@@ -370,6 +372,7 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       }
       bool inside = false;
       int kept = 0;  // logged forward: the entries some lane used, in list order
+      PH_BEGIN(ph_p)
       screen_accumulate<CH>(sc, sv, r, sm, count, lanes, wch, mc, base, dtf, Y, sums, inside,
                             [&](int32_t p, unsigned um) {
                               if constexpr (SAVE) {
@@ -379,15 +382,18 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
                               }
                             });
       if constexpr (SAVE) log_close(lo, kept);
+      PH_END(2, ph_p)
       nonempty = nonempty || inside;
       // AABB emptiness without a clearly-inside sample: the exact test over
       // this chunk of the list (a superset of the boxes the segment meets)
+      PH_BEGIN(ph_e)
       if (want && !nonempty)
         for (int i = 0; i < count; ++i)
           if (exact_aabb_overlap(sv, r, (int64_t)sm.list[i], seg.t0, seg.t1)) {
             nonempty = true;
             break;
           }
+      PH_END(4, ph_e)
       __syncwarp();
       if (cst.done) break;
       count = 0;
@@ -402,15 +408,19 @@ __device__ bool forward_segment_screened(const SceneView& sv, const BvhView& bv,
       log_samples(lo, mc, [&](int j) { return sums.get(j); });
     }
     // front-to-back compositing (renderer.py:230-239)
+    PH_BEGIN(ph_c)
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       const float4 a = sums.get(j);
       const float w3[3] = {a.y, a.z, a.w};
       acc.add_sample(j < mc ? a.x : 0.f, w3, (float)(tb + (double)j * seg.dt), dtf);
     }
+    PH_END(3, ph_c)
   }
   Counters<false> cnt;
+  PH_BEGIN(ph_x)
   emptiness_tail<false>(sv, bv, r, want, seg, nonempty, cnt, sm.ovf);
+  PH_END(7, ph_x)
   return nonempty;
 }
 
@@ -727,9 +737,9 @@ extern "C" int gsx_calibrate_sfu(int64_t iters, float* sink, double* ops, void* 
 
 #ifdef GSX_PHASE_PROF
 extern "C" int gsx_phase_times(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, gsx::g_phase, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, gsx::g_phase, sizeof(unsigned long long) * 24);
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[24] = {};
     cudaMemcpyToSymbol(gsx::g_phase, z, sizeof z);
   }
   return gsx_check_launch();

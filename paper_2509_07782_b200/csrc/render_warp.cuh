@@ -46,7 +46,7 @@ constexpr int WSTACK = GSX_WSTACK;  // warp traversal stack (shared memory)
 // nvcc -DGSX_PHASE_PROF); compiled out of the product library.
 #ifdef GSX_PHASE_PROF
 // one copy per translation unit (no -rdc); gsx_phase_times reads render.cu's
-static __device__ unsigned long long g_phase[16];
+static __device__ unsigned long long g_phase[24];
 #define PH_BEGIN(v) \
   __syncwarp();     \
   long long v = clock64();
@@ -738,6 +738,9 @@ struct Screen {
 // Held in shared memory instead of registers: at the 64-register cap of 32
 // warps per SM they lived in local memory (4 LDL + 4 STL per sample update,
 // missing L1 -- the dominant long-scoreboard stall of the r06 capture).
+#ifndef GSX_SCR_GEO_PF
+#define GSX_SCR_GEO_PF 0
+#endif
 #ifndef GSX_SCR_CH
 #define GSX_SCR_CH 16
 #endif
@@ -853,21 +856,36 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
   for (int b = 0; b < count; b += 32) {
     const int i = b + (int)lane;
     const int32_t pl = i < count ? sm.list[i] : 0;
+    PH_BEGIN(ph_s)
     const unsigned ml = i < count ? screen_entry(sc, pl) & lanes : 0u;
+    PH_END(16, ph_s)
+#if GSX_SCR_GEO_PF
+    // the batch's screened-in geometry blocks head for L1 together, one
+    // prefetch per lane, before the entries are set up one by one
+    if (ml) asm volatile("prefetch.global.L1 [%0];" ::"l"(sv.geo + 4 * (int64_t)pl));
+#endif
     unsigned todo = __ballot_sync(FULL, ml != 0u);
     unsigned mine = 0u;  // lanes that used this lane's entry
     while (todo) {
       const int e = __ffs(todo) - 1;
       todo &= todo - 1;
+      PH_CNT(21, 1)
       const unsigned m = __shfl_sync(FULL, ml, e);
       const int64_t p = __shfl_sync(FULL, pl, e);
+      PH_BEGIN(ph_u)
       const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
       const unsigned um = __ballot_sync(FULL, u.use);
+      PH_END(17, ph_u)
       if (lane == (unsigned)e) mine = um;
       if (!um) continue;
       float c[3] = {0.f, 0.f, 0.f};
+      PH_BEGIN(ph_r)
       if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
+      PH_END(18, ph_r)
+      PH_BEGIN(ph_m)
       qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
+      PH_END(19, ph_m)
+      PH_CNT(20, 1)
     }
     post(pl, mine);
   }

@@ -17,6 +17,7 @@ import paper_2509_07782_b200 as G  # noqa: E402
 from paper_2509_07782_b200 import _lib  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c3"
+variant = sys.argv[2] if len(sys.argv) > 2 else None
 rec, eps, cam_kw, cfg_kw, desc = bench.workload(cfgname)
 scene = G.Scene.from_records(rec)
 G.reorder_by_morton(scene)
@@ -24,22 +25,23 @@ cam = bench.make_camera(G, cam_kw)
 cfg = G.RenderConfig(**cfg_kw)
 L = _lib.lib()
 L.gsx_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 24)()
 for _ in range(2):
-    G.render(scene, cam, cfg)
+    G.render(scene, cam, cfg, variant=variant)
 torch.cuda.synchronize()
 L.gsx_phase_times(buf, 1)
 s = torch.cuda.current_stream()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(s)
-G.render(scene, cam, cfg)
+G.render(scene, cam, cfg, variant=variant)
 e1.record(s)
 torch.cuda.synchronize()
 L.gsx_phase_times(buf, 1)
-names = ["closest_hit(initial)", "warp_traverse", "list_process", "composite", "phantom/stats",
-         "advance(+ESS closest hit)", "march_total", "-"]
+names = ["closest_hit(initial)", "warp_traverse", "list_process", "composite",
+         "phantom/stats | exact emptiness over the list (screened)", "advance(+ESS closest hit)",
+         "march_total", "emptiness_tail (screened)"]
 tot = buf[6] or 1
-out = {n: {"warp_cycles": int(buf[i]), "share_of_march": buf[i] / tot} for i, n in enumerate(names[:7])}
+out = {n: {"warp_cycles": int(buf[i]), "share_of_march": buf[i] / tot} for i, n in enumerate(names)}
 warps = (cam.width * cam.height + 31) // 32
 counts = {"warp_node_steps": buf[8], "warp_list_entries": buf[9], "warp_iterations": buf[10],
           "lane_candidate_uses": buf[11], "lane_candidate_tests": buf[12], "reuses": buf[15],
@@ -54,5 +56,10 @@ counts = {"warp_node_steps": buf[8], "warp_list_entries": buf[9], "warp_iteratio
           "lanes_per_used_entry": buf[11] / max(buf[14], 1),
           "cycles_per_node_step": buf[1] / max(buf[8], 1),
           "cycles_per_list_entry": buf[2] / max(buf[9], 1)}
-print(json.dumps({"config": cfgname, "ms": e0.elapsed_time(e1), "phases": out, "counts": counts},
-                 indent=1))
+screened = {"screen (per batch)": buf[16], "setup (per screened-in entry)": buf[17],
+            "radiance (per used entry)": buf[18], "samples (per used entry)": buf[19]}
+screened = {k: {"warp_cycles": int(v), "share_of_march": v / tot} for k, v in screened.items()}
+counts["screened_in_entries"] = buf[21]
+counts["used_entries"] = buf[20]
+print(json.dumps({"config": cfgname, "ms": e0.elapsed_time(e1), "phases": out,
+                  "screened_list": screened, "counts": counts}, indent=1))
