@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
                       int64_t tile_begin, int64_t tile_stride, float* rgb, float* depth,
                       float* trans, const float4* view, void* log, long long log_nw) {
   constexpr int CH = GSX_SCR_CH;
-  using WS = std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmem>;
+  using WS = std::conditional_t<SMEM, WarpSmemA<CH>, WarpSmemT>;
   __shared__ WS smem[NT / 32];
   WS& sw = smem[threadIdx.x >> 5];
   const long long blk = (long long)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
@@ -485,6 +485,9 @@ __global__ void __launch_bounds__(NT, (SMEM ? GSX_SCR_MINB : GSX_SCRR_MINB) * 32
   Counters<false> cnt;
   LogWriter lw = log_writer(SAVE ? log : nullptr, blk);
   ovf_begin(sw);
+#if GSX_APP_TMA
+  app_barriers_init(sw);
+#endif
   march_warp<false, true>(sv, bv, r, hit, cfg, acc, cnt,
                           cfg.mode == 0 ? GSX_SYNC_FWD_U : GSX_SYNC_FWD, sw,
                           [&](const Seg& seg, bool want) {

@@ -77,6 +77,12 @@ struct Counters {
 #ifndef GSX_Y_SMEM
 #define GSX_Y_SMEM 0
 #endif
+#ifndef GSX_APP_TMA  // screened kernels: appearance blocks by TMA bulk copy (see app_issue)
+#define GSX_APP_TMA 1
+#endif
+#ifndef GSX_GEO_TMA  // ... and the geometry blocks (C3 24.1 vs 23.3 ms: the setup then
+#define GSX_GEO_TMA 0  // waits for a copy instead of a (mostly L1/L2-hit) broadcast load)
+#endif
 struct WarpSmem {
   int32_t stack[WSTACK];
   int32_t list[LCAP];
@@ -84,6 +90,19 @@ struct WarpSmem {
   float4 cone[5];  // packet cone (make_cone): (o, dlo^2), 4 x (plane normal, .w: dhi^2 | eps_scale | dlo | dhi)
 #if GSX_Y_SMEM == 1
   float ylane[9][32];  // per-lane SH basis (forward)
+#endif
+};
+
+// screened kernels: + the entry blocks the TMA engine stages (app_issue)
+struct WarpSmemT : WarpSmem {
+#if GSX_APP_TMA
+  float4 appb[2][GSX_APP_F4];   // the current and the next entry's appearance block
+  unsigned long long mbar[2];   // TMA completion barriers of the appearance blocks
+#if GSX_GEO_TMA
+  float4 geob[2][4];            // ... and geometry block
+  unsigned long long gbar[2];   // ... of the geometry blocks (waited on first)
+#endif
+  unsigned mpar;                // the barriers' phase parities (bit b: buffer b)
 #endif
 };
 
@@ -745,7 +764,7 @@ struct Screen {
 #define GSX_SCR_CH 16
 #endif
 template <int CH>
-struct WarpSmemA : WarpSmem {  // screened forward, sums in shared memory
+struct WarpSmemA : WarpSmemT {  // screened forward, sums in shared memory
   float4 acc[CH][32];
 };
 
@@ -846,13 +865,78 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
 // sets up only the entries whose mask holds it).  After each batch every
 // lane calls post(p, lanes that used p) for its entry (0: unused or beyond
 // the list; warp-converged: the logged forward compacts them with a ballot).
+#if GSX_APP_TMA
+// The radiance needs the entry's whole appearance block (368 B, the same for
+// every lane): loaded by the warp's lanes it costs a chain of L2 round trips
+// at 64 registers.  Instead lane 0 has the TMA engine copy it into a warp
+// buffer (cp.async.bulk, completion on an mbarrier) one entry ahead, while
+// the current entry is set up and evaluated; the lanes then read it from
+// shared memory.
+__device__ inline void app_barriers_init(WarpSmemT& sm) {
+  if ((threadIdx.x & 31) == 0) {
+    for (int b = 0; b < 2; ++b) {
+      const unsigned mb = (unsigned)__cvta_generic_to_shared(&sm.mbar[b]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+#if GSX_GEO_TMA
+      const unsigned gb = (unsigned)__cvta_generic_to_shared(&sm.gbar[b]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gb) : "memory");
+#endif
+    }
+    sm.mpar = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+// lane 0: buffer b <- primitive p's appearance block (and, GSX_GEO_TMA,
+// geometry block); the buffer's previous contents consumed
+__device__ inline void app_issue(WarpSmemT& sm, int b, const SceneView& sv, int64_t p) {
+  constexpr unsigned ABYTES = 16u * GSX_APP_F4, GBYTES = 64u;
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(&sm.mbar[b]);
+  const unsigned adst = (unsigned)__cvta_generic_to_shared(&sm.appb[b][0]);
+#if GSX_GEO_TMA
+  const unsigned gb = (unsigned)__cvta_generic_to_shared(&sm.gbar[b]);
+  const unsigned gdst = (unsigned)__cvta_generic_to_shared(&sm.geob[b][0]);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gb), "r"(GBYTES)
+               : "memory");
+#endif
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(ABYTES)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(adst),
+      "l"(sv.app + GSX_APP_F4 * p), "r"(ABYTES), "r"(mb)
+      : "memory");
+#if GSX_GEO_TMA
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(gdst),
+      "l"(sv.geo + 4 * p), "r"(GBYTES), "r"(gb)
+      : "memory");
+#else
+  (void)GBYTES;
+#endif
+}
+__device__ inline void bar_wait(const unsigned long long* bar, unsigned parity) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+#endif
+
 template <int CH, class YT, class Sums, class Post>
 __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, const RayCtx& r,
-                                         const WarpSmem& sm, int count, unsigned lanes,
+                                         WarpSmemT& sm, int count, unsigned lanes,
                                          bool want, int mc, const SegBase& base, float dtf, YT Y,
                                          Sums& sums, bool& inside, Post&& post) {
   const unsigned lane = threadIdx.x & 31;
   float qmn = 2.f;
+#if GSX_APP_TMA
+  unsigned par = sm.mpar;
+#endif
   for (int b = 0; b < count; b += 32) {
     const int i = b + (int)lane;
     const int32_t pl = i < count ? sm.list[i] : 0;
@@ -866,21 +950,60 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
 #endif
     unsigned todo = __ballot_sync(FULL, ml != 0u);
     unsigned mine = 0u;  // lanes that used this lane's entry
+#if GSX_APP_TMA
+    int bi = 0;
+    {
+      const int32_t p0 = __shfl_sync(FULL, pl, todo ? __ffs(todo) - 1 : 0);
+      if (todo && lane == 0) app_issue(sm, 0, sv, p0);
+    }
+#endif
     while (todo) {
       const int e = __ffs(todo) - 1;
       todo &= todo - 1;
       PH_CNT(21, 1)
       const unsigned m = __shfl_sync(FULL, ml, e);
       const int64_t p = __shfl_sync(FULL, pl, e);
+#if GSX_APP_TMA
+      {
+        // the next entry's block into the other buffer (its last reader was
+        // the previous iteration: every lane's reads ordered before the copy)
+        const int32_t pn = __shfl_sync(FULL, pl, todo ? __ffs(todo) - 1 : 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (todo && lane == 0) app_issue(sm, bi ^ 1, sv, pn);
+      }
+      const int bc = bi;  // this entry's buffer
+      const unsigned pc = (par >> bc) & 1u;
+      par ^= 1u << bc;
+      bi ^= 1;
+      PH_BEGIN(ph_u)
+#if GSX_GEO_TMA
+      bar_wait(&sm.gbar[bc], pc);
+      const CandUse u =
+          candidate_use_at<PlainLoad>(&sm.geob[bc][0], r, want && ((m >> lane) & 1u), mc, base,
+                                      dtf);
+#else
+      const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
+#endif
+#else
       PH_BEGIN(ph_u)
       const CandUse u = candidate_use(sv, r, p, want && ((m >> lane) & 1u), mc, base, dtf);
+#endif
       const unsigned um = __ballot_sync(FULL, u.use);
       PH_END(17, ph_u)
       if (lane == (unsigned)e) mine = um;
+#if GSX_APP_TMA
+      bar_wait(&sm.mbar[bc], pc);  // (both barriers complete a phase per use)
+      const float4* appp = &sm.appb[bc][0];
+#endif
       if (!um) continue;
       float c[3] = {0.f, 0.f, 0.f};
       PH_BEGIN(ph_r)
+#if GSX_APP_TMA
+      if (u.use) eval_radiance_f<PlainLoad, YT>(appp, Y, r.df, c);
+#else
       if (u.use) eval_radiance_f<LdgLoad, YT>(sv.app + GSX_APP_F4 * p, Y, r.df, c);
+#endif
       PH_END(18, ph_r)
       PH_BEGIN(ph_m)
       qmn = fminf(qmn, screened_samples<CH>(u, c, dtf, sums));
@@ -889,6 +1012,10 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
     }
     post(pl, mine);
   }
+#if GSX_APP_TMA
+  if (lane == 0) sm.mpar = par;
+  __syncwarp();
+#endif
   inside = inside || qmn <= 0.998f;
 }
 
