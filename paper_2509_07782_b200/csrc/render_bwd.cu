@@ -217,11 +217,15 @@ __device__ inline void sample_adjoint(RayAccum& acc, const PixelGrad& pg, float 
 // reduction buffer as soon as they are formed; lane L then sums rows L, L+32
 // of each half: direct rows go to atomics, the geometry / axis rows to the
 // batch (see the section comment above).
+// app: p's appearance block -- in global memory (the replay kernel) or staged
+// in the warp's shared buffer by a TMA bulk copy (the logged kernel)
+template <class L = LdgLoad>
 __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int64_t p, bool want,
                                       int mc, const SegBase& base, float dtf, const float* Y,
                                       const PixelGrad& pg, const float (&wos)[16],
                                       const float (&hh)[16], GradBatch& gb,
-                                      float* __restrict__ grad) {
+                                      float* __restrict__ grad, const float4* app = nullptr) {
+  if (!app) app = sv.app + GSX_APP_F4 * p;
   CandSetup cs;
   int jlo = 0, jhi = -1;
   bool use = want && mc > 0 && cand_setup(sv, r, p, base, cs) &&
@@ -230,7 +234,7 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
   const int lane = threadIdx.x & 31;
   float* col = gb.red + lane;
   float pre[3];
-  eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, r.df, pre, nullptr);
+  eval_radiance_pre<L>(app, Y, r.df, pre, nullptr);
   const float gcl =
       pg.gC[0] * fmaxf(pre[0], 0.f) + pg.gC[1] * fmaxf(pre[1], 0.f) + pg.gC[2] * fmaxf(pre[2], 0.f);
   const float nkl2 = -cs.kl2;
@@ -294,13 +298,13 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
   __syncwarp();
   // half B: spherical-Gaussian lobes, one at a time (rolled: keeps the 14
   // float4 of lobe data out of registers); the lobe value is recomputed
-  const float4* ap = sv.app + GSX_APP_F4 * p;
+  const float4* ap = app;
 #pragma unroll 1
   for (int l0 = 0; l0 < 7; l0 += SG_GROUP) {
     const int nl = min(SG_GROUP, 7 - l0);
 #pragma unroll 1
     for (int l = l0; l < l0 + nl; ++l) {
-      const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
+      const float4 ax = L()(ap + 9 + 2 * l), am = L()(ap + 10 + 2 * l);
       const float cs2 = fmaf(ax.x, r.df[0], fmaf(ax.y, r.df[1], ax.z * r.df[2]));
       const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
       const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
@@ -789,9 +793,11 @@ struct BwdlShape<true> {
   static constexpr int threads = GSX_BWDP_THREADS, minb = GSX_BWDP_MINB,
                        warp_floats = PAIR_WARP_FLOATS;
 };
+// entries path: + two staged appearance blocks and their barriers per warp
+constexpr int ENTRY_TMA_FLOATS = 2 * 4 * GSX_APP_F4 + 8;
 template <>
 struct BwdlShape<false> {
-  static constexpr int threads = 128, minb = 4, warp_floats = BWD_WARP_FLOATS;
+  static constexpr int threads = 128, minb = 4, warp_floats = BWD_WARP_FLOATS + ENTRY_TMA_FLOATS;
 };
 __device__ inline bool log_wants_pairs(const char* log, const gsx_render_cfg& cfg) {
   if (cfg.pass2 != 0) return cfg.pass2 == 1;
@@ -823,6 +829,19 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
                        : GradBatch{wsm, wsm + RED_FLOATS, 0};
   float Y[PAIRS ? 1 : 9];
   if constexpr (!PAIRS) sh_basis_f(r.df, Y);
+  // entries path: each entry's appearance block is staged by a TMA bulk copy
+  // one entry ahead (as in the screened forward, render_warp.cuh app_issue)
+  float4* appb = (float4*)(wsm + BWD_WARP_FLOATS);  // [2][GSX_APP_F4]
+  unsigned long long* abar = (unsigned long long*)(appb + 2 * GSX_APP_F4);
+  unsigned apar = 0u;
+  if constexpr (!PAIRS) {
+    if (lane == 0) {
+      tma_bar_init(&abar[0]);
+      tma_bar_init(&abar[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   long long off = log_first((void*)log)[wid];
   while (off >= 0) {
     const long long start = off;
@@ -918,11 +937,25 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
         for (int i0 = 0; i0 < count; i0 += 32) {
           const int ent = i0 + lane < count ? __ldcs(list + i0 + lane) : 0;
           const int nb = min(32, count - i0);
-          // (an L1 prefetch of entry k + 1 / k + 2's geometry and appearance
-          // measured slower: 13.15 vs 12.58 ms on C2)
-          for (int k = 0; k < nb; ++k)
-            grad_candidate(sv, r, (int64_t)__shfl_sync(FULL, ent, k), mc > 0, mc, base, dtf, Y,
-                           pg, wos, hh, gb, grad);
+          constexpr unsigned ABYTES = 16u * GSX_APP_F4;
+          {
+            const int p0 = __shfl_sync(FULL, ent, 0);
+            if (lane == 0) tma_copy(appb, sv.app + GSX_APP_F4 * (int64_t)p0, ABYTES, &abar[0]);
+          }
+          for (int k = 0; k < nb; ++k) {
+            const int bk = k & 1;
+            const int pn = __shfl_sync(FULL, ent, k + 1 < nb ? k + 1 : k);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (k + 1 < nb && lane == 0)
+              tma_copy(appb + GSX_APP_F4 * (bk ^ 1), sv.app + GSX_APP_F4 * (int64_t)pn, ABYTES,
+                       &abar[bk ^ 1]);
+            bar_wait(&abar[bk], (apar >> bk) & 1u);
+            apar ^= 1u << bk;
+            grad_candidate<PlainLoad>(sv, r, (int64_t)__shfl_sync(FULL, ent, k), mc > 0, mc,
+                                      base, dtf, Y, pg, wos, hh, gb, grad,
+                                      appb + GSX_APP_F4 * bk);
+          }
         }
       }
       if (o == off) break;

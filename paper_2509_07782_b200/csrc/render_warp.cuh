@@ -916,6 +916,24 @@ __device__ inline void app_issue(WarpSmemT& sm, int b, const SceneView& sv, int6
   (void)GBYTES;
 #endif
 }
+// generic forms (raw shared-memory pointers): barrier init, one bulk copy
+// global -> shared completing on `bar`
+__device__ inline void tma_bar_init(unsigned long long* bar) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+}
+__device__ inline void tma_copy(void* dst, const void* src, unsigned bytes,
+                                unsigned long long* bar) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(d),
+      "l"(src), "r"(bytes), "r"(mb)
+      : "memory");
+}
 __device__ inline void bar_wait(const unsigned long long* bar, unsigned parity) {
   const unsigned mb = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(
