@@ -757,9 +757,6 @@ struct Screen {
 // Held in shared memory instead of registers: at the 64-register cap of 32
 // warps per SM they lived in local memory (4 LDL + 4 STL per sample update,
 // missing L1 -- the dominant long-scoreboard stall of the r06 capture).
-#ifndef GSX_SCR_GEO_PF
-#define GSX_SCR_GEO_PF 0
-#endif
 #ifndef GSX_SCR_CH
 #define GSX_SCR_CH 16
 #endif
@@ -961,11 +958,6 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
     PH_BEGIN(ph_s)
     const unsigned ml = i < count ? screen_entry(sc, pl) & lanes : 0u;
     PH_END(16, ph_s)
-#if GSX_SCR_GEO_PF
-    // the batch's screened-in geometry blocks head for L1 together, one
-    // prefetch per lane, before the entries are set up one by one
-    if (ml) asm volatile("prefetch.global.L1 [%0];" ::"l"(sv.geo + 4 * (int64_t)pl));
-#endif
     unsigned todo = __ballot_sync(FULL, ml != 0u);
     unsigned mine = 0u;  // lanes that used this lane's entry
 #if GSX_APP_TMA
