@@ -80,6 +80,9 @@ struct Counters {
 #ifndef GSX_APP_TMA  // screened kernels: appearance blocks by TMA bulk copy (see app_issue)
 #define GSX_APP_TMA 1
 #endif
+#ifndef GSX_APP_NB  // staging buffers per warp: entries are staged GSX_APP_NB - 1 ahead
+#define GSX_APP_NB 2  // (3 / 4: C3 24.7 / 25.2 vs 23.4 ms -- copies for entries no lane uses)
+#endif
 #ifndef GSX_GEO_TMA  // ... and the geometry blocks (C3 24.1 vs 23.3 ms: the setup then
 #define GSX_GEO_TMA 0  // waits for a copy instead of a (mostly L1/L2-hit) broadcast load)
 #endif
@@ -96,11 +99,11 @@ struct WarpSmem {
 // screened kernels: + the entry blocks the TMA engine stages (app_issue)
 struct WarpSmemT : WarpSmem {
 #if GSX_APP_TMA
-  float4 appb[2][GSX_APP_F4];   // the current and the next entry's appearance block
-  unsigned long long mbar[2];   // TMA completion barriers of the appearance blocks
+  float4 appb[GSX_APP_NB][GSX_APP_F4];  // the current and the next entries' appearance blocks
+  unsigned long long mbar[GSX_APP_NB];  // TMA completion barriers of the appearance blocks
 #if GSX_GEO_TMA
-  float4 geob[2][4];            // ... and geometry block
-  unsigned long long gbar[2];   // ... of the geometry blocks (waited on first)
+  float4 geob[GSX_APP_NB][4];           // ... and geometry blocks
+  unsigned long long gbar[GSX_APP_NB];  // ... of the geometry blocks (waited on first)
 #endif
   unsigned mpar;                // the barriers' phase parities (bit b: buffer b)
 #endif
@@ -871,7 +874,7 @@ __device__ inline float screened_samples(const CandUse& u, const float* c, float
 // shared memory.
 __device__ inline void app_barriers_init(WarpSmemT& sm) {
   if ((threadIdx.x & 31) == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < GSX_APP_NB; ++b) {
       const unsigned mb = (unsigned)__cvta_generic_to_shared(&sm.mbar[b]);
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
 #if GSX_GEO_TMA
@@ -961,10 +964,16 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
     unsigned todo = __ballot_sync(FULL, ml != 0u);
     unsigned mine = 0u;  // lanes that used this lane's entry
 #if GSX_APP_TMA
+    constexpr int NB = GSX_APP_NB, D = GSX_APP_NB - 1;  // buffers, staging distance
     int bi = 0;
     {
-      const int32_t p0 = __shfl_sync(FULL, pl, todo ? __ffs(todo) - 1 : 0);
-      if (todo && lane == 0) app_issue(sm, 0, sv, p0);
+      unsigned t = todo;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int32_t pd = __shfl_sync(FULL, pl, t ? __ffs(t) - 1 : 0);
+        if (t && lane == 0) app_issue(sm, d, sv, pd);
+        t &= t - 1;
+      }
     }
 #endif
     while (todo) {
@@ -975,17 +984,20 @@ __device__ inline void screen_accumulate(const Screen& sc, const SceneView& sv, 
       const int64_t p = __shfl_sync(FULL, pl, e);
 #if GSX_APP_TMA
       {
-        // the next entry's block into the other buffer (its last reader was
-        // the previous iteration: every lane's reads ordered before the copy)
-        const int32_t pn = __shfl_sync(FULL, pl, todo ? __ffs(todo) - 1 : 0);
+        // the entry D ahead into the buffer the previous iteration read
+        // (every lane's reads ordered before the copy)
+        unsigned t = todo;
+#pragma unroll
+        for (int d = 1; d < D; ++d) t &= t - 1;
+        const int32_t pn = __shfl_sync(FULL, pl, t ? __ffs(t) - 1 : 0);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (todo && lane == 0) app_issue(sm, bi ^ 1, sv, pn);
+        if (t && lane == 0) app_issue(sm, (bi + D) % NB, sv, pn);
       }
       const int bc = bi;  // this entry's buffer
       const unsigned pc = (par >> bc) & 1u;
       par ^= 1u << bc;
-      bi ^= 1;
+      bi = bi + 1 == NB ? 0 : bi + 1;
       PH_BEGIN(ph_u)
 #if GSX_GEO_TMA
       bar_wait(&sm.gbar[bc], pc);
