@@ -22,18 +22,22 @@ rec, eps, cam_kw, cfg_kw, desc = bench.workload(cfgname)
 scene = G.Scene.from_records(rec)
 G.reorder_by_morton(scene)
 cam = bench.make_camera(G, cam_kw)
+log = None
+if len(sys.argv) > 3 and sys.argv[3] == "logged":  # the training forward
+    from paper_2509_07782_b200.renderer import MarchLog
+    log = MarchLog(cam)
 cfg = G.RenderConfig(**cfg_kw)
 L = _lib.lib()
 L.gsx_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 24)()
 for _ in range(2):
-    G.render(scene, cam, cfg, variant=variant)
+    G.render(scene, cam, cfg, variant=variant, log=log)
 torch.cuda.synchronize()
 L.gsx_phase_times(buf, 1)
 s = torch.cuda.current_stream()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(s)
-G.render(scene, cam, cfg, variant=variant)
+G.render(scene, cam, cfg, variant=variant, log=log)
 e1.record(s)
 torch.cuda.synchronize()
 L.gsx_phase_times(buf, 1)
