@@ -542,7 +542,10 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
       const unsigned ends = __ballot_sync(FULL, valid && (lane == last || en != e));
       const int nrun = __popc(ends);
       b0 = bend;
+      PH_BEGIN(ph_f)
       if (gb.n + nrun > PAIR_RUNS) grad_batch_flush(sv, gb, grad);
+      PH_END(6, ph_f)
+      PH_BEGIN(ph_su)
 
       // ---- the pair: setup, radiance, moments (renderer.py:207-240 adjoint)
       const float* lt = pb.lt + src;
@@ -566,7 +569,11 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
                        sample_range(cs, dtf, mc, jlo, jhi);
       const YDir Y{rr.df};
       float pre[3] = {0.f, 0.f, 0.f};
+      PH_END(1, ph_su)
+      PH_BEGIN(ph_ra)
       if (use) eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, rr.df, pre, nullptr);
+      PH_END(2, ph_ra)
+      PH_BEGIN(ph_mo)
       const float gcl = gC[0] * fmaxf(pre[0], 0.f) + gC[1] * fmaxf(pre[1], 0.f) +
                         gC[2] * fmaxf(pre[2], 0.f);
       float m0 = 0.f, m1 = 0.f, m2 = 0.f, e0 = 0.f;
@@ -595,6 +602,8 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
       float* const gb_bat = gb.bat;
       const int nb = gb.n;
 
+      PH_END(3, ph_mo)
+      PH_BEGIN(ph_p1)
       // ---- P1: geometry moments + SH 0-21
       {
         const float4 g0 = __ldg(sv.geo + 4 * p);
@@ -625,6 +634,8 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
         }
       });
 
+      PH_END(4, ph_p1)
+      PH_BEGIN(ph_p2)
       // ---- P2 / P3: spherical-Gaussian lobes (+ the last 5 SH values in P3)
       const float4* ap = sv.app + GSX_APP_F4 * p;
 #pragma unroll 1
@@ -634,6 +645,7 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
 #pragma unroll
           for (int idx = 22; idx < 27; ++idx) col[(idx - 22) * PR_ROW] = Y[idx / 3] * gpc[idx % 3];
         }
+        PH_BEGIN(ph_lc)
 #pragma unroll 1
         for (int l = lb0; l < lb0 + nl; ++l) {
           float* c = col + (r0 + 7 * (l - lb0)) * PR_ROW;
@@ -655,6 +667,8 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
             for (int k = 0; k < 7; ++k) c[k * PR_ROW] = 0.f;
           }
         }
+        PH_END(10, ph_lc)
+        PH_BEGIN(ph_lr)
         pair_reduce(pb, ends, pe, r0 + 7 * nl, [&](int row, float sum, int64_t ps, int run) {
           if (row < r0) {
             if (sum != 0.f) atomicAdd(grad + (int64_t)GSX_NREC * ps + 11 + 22 + row, sum);
@@ -667,7 +681,10 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
             atomicAdd(grad + (int64_t)GSX_NREC * ps + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)),
                       sum);
         });
+        PH_END(11, ph_lr)
       }
+      PH_END(5, ph_p2)
+      PH_CNT(9, 1)
       gb.n = nb + nrun;
     }
   }
@@ -870,6 +887,7 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
       dt = __ldcs((const double*)(body + Lo.dt) + slot);
       mc = __ldcs((const int*)(body + Lo.mc) + slot);
     }
+    PH_BEGIN(ph_pro)
     const float4* smp = (const float4*)(body + Lo.smp) + (h->swidth ? lane : slot);
     const int nact = sw;  // the sample array's row stride
     const float dtf = (float)dt;
@@ -907,6 +925,7 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
       }
     }
 #endif
+    PH_END(0, ph_pro)
     const SegBase base = seg_base(r, tb);
     if constexpr (PAIRS) {
       // the lane table and adjoints of this record for the pair lanes
@@ -972,6 +991,17 @@ __global__ void __launch_bounds__(BwdlShape<PAIRS>::threads, BwdlShape<PAIRS>::m
 }
 
 }  // namespace
+
+#ifdef GSX_PHASE_PROF
+extern "C" int gsx_phase_times_bwd(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, gsx::g_phase, sizeof(unsigned long long) * 24);
+  if (reset) {
+    unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(gsx::g_phase, z, sizeof z);
+  }
+  return gsx_check_launch();
+}
+#endif
 
 constexpr int BWD_SMEM = (BWD_THREADS / 32) * BWD_WARP_FLOATS * (int)sizeof(float);
 template <bool PAIRS>
