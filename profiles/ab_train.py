@@ -60,6 +60,10 @@ for screen in (False, True):
     res[key + "_bwd_logged_ms"] = timed(bwd)
     g = tr.grad.clone()
     res[key + "_grad_norm"] = float(g.norm())
+    for p2, p2name in ((1, "pairs"), (2, "entries")):  # forced pass-2 strategy
+        res[key + "_bwd_logged_" + p2name + "_ms"] = timed(
+            lambda: G.render_backward(scene, cam, cfg, tr.rgb, tr.depth, tr.trans, tr.dI,
+                                      grad=tr.grad, log=tr.log, pass2=p2))
 res["fwd_unlogged_ms"] = timed(lambda: G.render(scene, cam, cfg))
 res["step_ms"] = timed(lambda: tr.step(target))
 print(json.dumps(res), flush=True)
