@@ -38,8 +38,10 @@ struct PixelGrad {
 // a shared buffer (row = value, column = lane; rows padded to 36 floats: the
 // column writes hit banks (4 row + lane) mod 32 and the row sums read 16-byte
 // vectors conflict-free per quarter warp).  Rows, in two halves:
-//   A (37 rows): 0-9 geometry moments, 10-36 SH (b, c) -> record 11 + 3b + c
-//   B (49 rows): lobe l at 7l: raw axis sum (3), sharpness, amplitude (3)
+//   A (32 rows): 0-9 geometry moments, 10-31 SH (b, c) 0-21 -> record 11 + 3b + c
+//   B (49 + 5 rows): lobe l at 7l: raw axis sum (3), sharpness, amplitude (3);
+//     SH 22-26 at 7 SG_GROUP (written with half A, summed in the first lobe
+//     pass: 3 row passes per candidate instead of 4)
 // Geometry enters only through the moment tensors of the lane offsets
 // v = xc - mu and the direction d, with xc the ray's point of closest
 // approach to the primitive (t_c of the setup) and the moments taken in
@@ -59,7 +61,7 @@ struct PixelGrad {
 // issues its atomics -- the per-lane geometry work of the old formulation
 // (~240 instructions per candidate) becomes ~45 + 1/32 of the finish.
 constexpr int RED_ROW = 36;
-constexpr int RED_ROWS_A = 37;
+constexpr int RED_ROWS_A = 32;
 // half B in lobe groups of SG_GROUP (7: one pass of 49 rows; 4: two passes of
 // 28 and 21 rows, so the buffer is sized by half A and a CTA needs 15% less
 // shared memory).  Logged backward, C2 ms (profiles/time_bwd_variants.py):
@@ -70,7 +72,8 @@ constexpr int RED_ROWS_A = 37;
 #define GSX_BWD_SG_GROUP 7
 #endif
 constexpr int SG_GROUP = GSX_BWD_SG_GROUP;
-constexpr int RED_ROWS_B = 7 * SG_GROUP;
+constexpr int SH_TAIL_ROW = 7 * SG_GROUP;  // SH values 22-26
+constexpr int RED_ROWS_B = 7 * SG_GROUP + 5;
 constexpr int RED_FLOATS = (RED_ROWS_B > RED_ROWS_A ? RED_ROWS_B : RED_ROWS_A) * RED_ROW;
 constexpr int BAT_ROW = 33;                        // 31 values + candidate id, padded
 constexpr int BAT_FLOATS = 32 * BAT_ROW;
@@ -282,12 +285,16 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
 #pragma unroll
   for (int bsh = 0; bsh < 9; ++bsh)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) col[(10 + 3 * bsh + c) * RED_ROW] = Y[bsh] * gpc[c];
+    for (int c = 0; c < 3; ++c) {
+      const int idx = 3 * bsh + c;
+      col[(idx < 22 ? 10 + idx : SH_TAIL_ROW + idx - 22) * RED_ROW] = Y[bsh] * gpc[c];
+    }
   // half A: geometry moments -> batch, SH -> atomics
   float* gdst = grad + (int64_t)GSX_NREC * p;
   float* brow = gb.bat + gb.n * BAT_ROW;
   __syncwarp();
-  for (int row = lane; row < RED_ROWS_A; row += 32) {
+  {
+    const int row = lane;
     const float sum = row_sum(gb.red, row);
     if (row < 10)
       brow[row] = sum;
@@ -319,10 +326,12 @@ __device__ inline void grad_candidate(const SceneView& sv, const RayCtx& r, int6
       c[6 * RED_ROW] = lb * gpc[2];
     }
     __syncwarp();
-    for (int row = lane; row < 7 * nl; row += 32) {
+    for (int row = lane; row < 7 * nl + (l0 == 0 ? 5 : 0); row += 32) {
       const float sum = row_sum(gb.red, row);
       const int l = l0 + row / 7, k = row % 7;
-      if (k < 3)
+      if (row >= 7 * nl) {  // SH 22-26 (first pass only)
+        if (sum != 0.f) atomicAdd(gdst + 11 + 22 + (row - 7 * nl), sum);
+      } else if (k < 3)
         brow[10 + 3 * l + k] = sum;
       else if (sum != 0.f)
         atomicAdd(gdst + (k == 3 ? 59 + l : 66 + 3 * l + (k - 4)), sum);
