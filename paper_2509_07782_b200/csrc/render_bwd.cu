@@ -442,9 +442,6 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
 // An entry split by a 32-pair boundary contributes two batch rows; every
 // finished value is linear in them, so the atomics add up the same.
 // ---------------------------------------------------------------------------
-#ifndef GSX_BWDP_LCACHE
-#define GSX_BWDP_LCACHE 1  // keep the lobe terms in registers from the radiance pass
-#endif
 constexpr int PR_ROW = 36;  // a row per lane, 32 pair columns (16-byte rows: float4 reads conflict-free)
 constexpr int PR_FLOATS = 32 * PR_ROW;
 constexpr int LT_ROWS = 14;  // lane table: df[3], base.hi[3], base.lo[3], dtf, mc, gC[3]
@@ -474,6 +471,51 @@ __device__ inline int nth_bit(unsigned m, int n) {
     }
   }
   return pos;
+}
+
+// Radiance of one pair's primitive (eval_radiance_pre's arithmetic, so `pre`
+// is the same) keeping, per lobe, what the lobe gradient columns need: e*w,
+// e*(cs2-1), e and am.gC with the radiance clamp applied.  Reloading them in
+// the lobe pass cost 30% of the pair kernel (L1 is nearly all shared memory
+// there, so every reload was an L2 round trip).
+struct LobeTerms {
+  float w[7], c[7], v[7], g[7];
+};
+__device__ inline void radiance_lobe_terms(const float4* __restrict__ app, const YDir& Y,
+                                           const float* d, const float* gC, float* pre,
+                                           LobeTerms& lt) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    const float4 v = __ldg(app + b);
+    s0 = fmaf(Y[b], v.x, s0);
+    s1 = fmaf(Y[b], v.y, s1);
+    s2 = fmaf(Y[b], v.z, s2);
+  }
+#pragma unroll
+  for (int l = 0; l < 7; ++l) {
+    const float4 ax = __ldg(app + 9 + 2 * l), am = __ldg(app + 10 + 2 * l);
+    const float cs2 = fmaf(ax.x, d[0], fmaf(ax.y, d[1], ax.z * d[2]));
+    const float e = __expf(ax.w * (cs2 - 1.0f));
+    s0 = fmaf(e, am.x, s0);
+    s1 = fmaf(e, am.y, s1);
+    s2 = fmaf(e, am.z, s2);
+    lt.v[l] = e;
+    lt.w[l] = e * ax.w;
+    lt.c[l] = e * (cs2 - 1.f);
+    lt.g[l] = am.x * gC[0] + am.y * gC[1] + am.z * gC[2];
+  }
+  pre[0] = s0;
+  pre[1] = s1;
+  pre[2] = s2;
+  if (!(s0 > 0.f && s1 > 0.f && s2 > 0.f)) {  // a clamped channel: rare
+#pragma unroll
+    for (int l = 0; l < 7; ++l) {
+      const float4 am = __ldg(app + 10 + 2 * l);
+      lt.g[l] = (s0 > 0.f ? am.x * gC[0] : 0.f) + (s1 > 0.f ? am.y * gC[1] : 0.f) +
+                (s2 > 0.f ? am.z * gC[2] : 0.f);
+    }
+  }
 }
 
 // Sum rows [0, nrows) of the pass buffer over each run of `ends` (bit k set:
@@ -583,52 +625,13 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
       float pre[3] = {0.f, 0.f, 0.f};
       PH_END(1, ph_su)
       PH_BEGIN(ph_ra)
-#if GSX_BWDP_LCACHE
-      // radiance, keeping what the lobe columns need in registers so P2/P3
-      // do not reload the appearance block: e*w, e*(cs2-1), e and am.gC
-      // (same arithmetic as eval_radiance_pre for pre)
-      float lw[7], lc[7], lv[7], lg[7];
+      LobeTerms lobe;
       if (use) {
-        const float4* ap0 = sv.app + GSX_APP_F4 * p;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-        for (int b = 0; b < 9; ++b) {
-          const float4 v = __ldg(ap0 + b);
-          s0 = fmaf(Y[b], v.x, s0);
-          s1 = fmaf(Y[b], v.y, s1);
-          s2 = fmaf(Y[b], v.z, s2);
-        }
-#pragma unroll
-        for (int l = 0; l < 7; ++l) {
-          const float4 ax = __ldg(ap0 + 9 + 2 * l), am = __ldg(ap0 + 10 + 2 * l);
-          const float cs2 = fmaf(ax.x, rr.df[0], fmaf(ax.y, rr.df[1], ax.z * rr.df[2]));
-          const float e = __expf(ax.w * (cs2 - 1.0f));
-          s0 = fmaf(e, am.x, s0);
-          s1 = fmaf(e, am.y, s1);
-          s2 = fmaf(e, am.z, s2);
-          lv[l] = e;
-          lw[l] = e * ax.w;
-          lc[l] = e * (cs2 - 1.f);
-          lg[l] = am.x * gC[0] + am.y * gC[1] + am.z * gC[2];
-        }
-        pre[0] = s0;
-        pre[1] = s1;
-        pre[2] = s2;
-        if (!(s0 > 0.f && s1 > 0.f && s2 > 0.f)) {  // a clamped channel: rare
-#pragma unroll
-          for (int l = 0; l < 7; ++l) {
-            const float4 am = __ldg(ap0 + 10 + 2 * l);
-            lg[l] = (s0 > 0.f ? am.x * gC[0] : 0.f) + (s1 > 0.f ? am.y * gC[1] : 0.f) +
-                    (s2 > 0.f ? am.z * gC[2] : 0.f);
-          }
-        }
+        radiance_lobe_terms(sv.app + GSX_APP_F4 * p, Y, rr.df, gC, pre, lobe);
       } else {
 #pragma unroll
-        for (int l = 0; l < 7; ++l) lw[l] = lc[l] = lv[l] = lg[l] = 0.f;
+        for (int l = 0; l < 7; ++l) lobe.w[l] = lobe.c[l] = lobe.v[l] = lobe.g[l] = 0.f;
       }
-#else
-      if (use) eval_radiance_pre(sv.app + GSX_APP_F4 * p, Y, rr.df, pre, nullptr);
-#endif
       PH_END(2, ph_ra)
       PH_BEGIN(ph_mo)
       const float gcl = gC[0] * fmaxf(pre[0], 0.f) + gC[1] * fmaxf(pre[1], 0.f) +
@@ -693,13 +696,9 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
 
       PH_END(4, ph_p1)
       PH_BEGIN(ph_p2)
-      // ---- P2 / P3: spherical-Gaussian lobes (+ the last 5 SH values in P3)
-#if GSX_BWDP_LCACHE
+      // ---- P2 / P3: spherical-Gaussian lobes (+ the last 5 SH values in P3),
+      // from the lobe terms of the radiance pass (zero when !use: e0 = gpc = 0)
 #pragma unroll
-#else
-      const float4* ap = sv.app + GSX_APP_F4 * p;
-#pragma unroll 1
-#endif
       for (int pass = 0; pass < 2; ++pass) {
         const int lb0 = pass == 0 ? 0 : 4, nl = pass == 0 ? 4 : 3, r0 = pass == 0 ? 0 : 5;
         if (pass == 1) {
@@ -707,42 +706,18 @@ __device__ void pair_pass(const SceneView& sv, const PairBufs& pb, GradBatch& gb
           for (int idx = 22; idx < 27; ++idx) col[(idx - 22) * PR_ROW] = Y[idx / 3] * gpc[idx % 3];
         }
         PH_BEGIN(ph_lc)
-#if GSX_BWDP_LCACHE
 #pragma unroll
         for (int l = lb0; l < lb0 + nl; ++l) {
           float* c = col + (r0 + 7 * (l - lb0)) * PR_ROW;
-          const float ga = lg[l] * e0, f = lw[l] * ga;
+          const float ga = lobe.g[l] * e0, f = lobe.w[l] * ga;
           c[0] = f * rr.df[0];
           c[PR_ROW] = f * rr.df[1];
           c[2 * PR_ROW] = f * rr.df[2];
-          c[3 * PR_ROW] = lc[l] * ga;
-          c[4 * PR_ROW] = lv[l] * gpc[0];
-          c[5 * PR_ROW] = lv[l] * gpc[1];
-          c[6 * PR_ROW] = lv[l] * gpc[2];
+          c[3 * PR_ROW] = lobe.c[l] * ga;
+          c[4 * PR_ROW] = lobe.v[l] * gpc[0];
+          c[5 * PR_ROW] = lobe.v[l] * gpc[1];
+          c[6 * PR_ROW] = lobe.v[l] * gpc[2];
         }
-#else
-#pragma unroll 1
-        for (int l = lb0; l < lb0 + nl; ++l) {
-          float* c = col + (r0 + 7 * (l - lb0)) * PR_ROW;
-          if (use) {
-            const float4 ax = __ldg(ap + 9 + 2 * l), am = __ldg(ap + 10 + 2 * l);
-            const float cs2 = fmaf(ax.x, rr.df[0], fmaf(ax.y, rr.df[1], ax.z * rr.df[2]));
-            const float lb = __expf(ax.w * (cs2 - 1.0f));  // == eval_radiance_pre's lobe value
-            const float ga = am.x * gpc[0] + am.y * gpc[1] + am.z * gpc[2];
-            const float f = lb * ax.w * ga;
-            c[0] = f * rr.df[0];
-            c[PR_ROW] = f * rr.df[1];
-            c[2 * PR_ROW] = f * rr.df[2];
-            c[3 * PR_ROW] = lb * (cs2 - 1.f) * ga;
-            c[4 * PR_ROW] = lb * gpc[0];
-            c[5 * PR_ROW] = lb * gpc[1];
-            c[6 * PR_ROW] = lb * gpc[2];
-          } else {
-#pragma unroll
-            for (int k = 0; k < 7; ++k) c[k * PR_ROW] = 0.f;
-          }
-        }
-#endif
         PH_END(10, ph_lc)
         PH_BEGIN(ph_lr)
         pair_reduce(pb, ends, pe, r0 + 7 * nl, [&](int row, float sum, int64_t ps, int run) {
