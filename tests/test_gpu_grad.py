@@ -143,3 +143,22 @@ def test_backward_march_log_c1(pass2):
     cam = G.orbit_cameras(1, radius=3.0, focal=64.0, width=32, height=32)[0]
     g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive"), log="full", pass2=pass2)
     _compare(g, gref)
+
+
+@pytest.mark.parametrize("pass2", [1, 2])
+def test_backward_march_log_clamped_channels(pass2):
+    """Primitives whose radiance is clamped at 0 in some channels (large
+    negative SH DC terms on every other primitive, a different channel each):
+    the clamp masks the lobe / SH gradients of those channels, which the pair
+    path applies after its register-cached radiance pass (radiance_lobe_terms)."""
+    import paper_2509_07782_b200 as G
+
+    rec = gen_test_scene_records("random-cloud", count=300, seed=7, anisotropy=3.0,
+                                 base_scale=0.05)
+    for i in range(0, rec.shape[0], 2):
+        rec[i, 11 + (i // 2) % 3] = -4.0  # SH basis 0, channel c -> record 11 + c
+    rec = f32_records(rec)
+    cam = G.orbit_cameras(2, radius=3.0, focal=40.0, width=40, height=24)[1]
+    g, gref = _run(G, rec, 0.01, cam, dict(mode="adaptive", background=(0.2, 0.5, 0.9)),
+                   log="full", pass2=pass2)
+    _compare(g, gref)
