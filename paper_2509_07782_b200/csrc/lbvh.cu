@@ -83,15 +83,30 @@ __device__ inline Box node_union(const float4* nodes, int32_t c) {
   return r;
 }
 
+#ifndef GSX_REFIT_ACQREL  // 0: the SC-fenced arrival (3M rebuild 2.60 vs 2.51 ms)
+#define GSX_REFIT_ACQREL 1
+#endif
 __global__ void k_refit(const float* __restrict__ box32, int64_t n, float4* nodes,
                         const int32_t* __restrict__ parents, int32_t* flags) {
   int64_t leaf = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (leaf >= n) return;
   int32_t p = parents[(n - 1) + leaf];
   while (p >= 0) {
+#if GSX_REFIT_ACQREL
+    // one acquire-release arrival instead of two SC fences: the first
+    // arrival's node stores are released by its increment, the second
+    // arrival acquires them through the same counter
+    int32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                 : "=r"(old)
+                 : "l"(flags + p)
+                 : "memory");
+    if (old == 0) return;  // first arrival: sibling not ready
+#else
     __threadfence();
     if (atomicAdd(&flags[p], 1) == 0) return;  // first arrival: sibling not ready
     __threadfence();
+#endif
     float4* nd = nodes + 4 * (int64_t)p;
     int32_t cl = __float_as_int(__ldcg(&nd[0].w)), cr = __float_as_int(__ldcg(&nd[1].w));
     Box bl = cl < 0 ? leaf_box(box32, ~cl) : node_union(nodes, cl);
