@@ -221,9 +221,15 @@ __device__ inline float half_area(const float4& lo, const float4& hi) {
   return dx * dy + dy * dz + dz * dx;
 }
 
+// GSX_GREEDY_BASE: a level's new BVH4 slots are base + (its queue index), with
+// base = the slots used before the level, so one atomic per child assigns
+// both (0: a second counter for the slots)
+#ifndef GSX_GREEDY_BASE
+#define GSX_GREEDY_BASE 1
+#endif
 __device__ inline void greedy_item(const float4* __restrict__ nodes, const QItem it,
                                    QItem* __restrict__ qout, uint32_t* nout_p, uint32_t* n4_p,
-                                   float4* __restrict__ nodes4) {
+                                   uint32_t base, float4* __restrict__ nodes4) {
   {
     float4 lo[4], hi[4];
     int32_t ref[4];
@@ -273,8 +279,14 @@ __device__ inline void greedy_item(const float4* __restrict__ nodes, const QItem
       } else if (ref[k] < 0) {
         ch[k] = ref[k];
       } else {
-        const uint32_t slot = atomicAdd(n4_p, 1u);
-        qout[atomicAdd(nout_p, 1u)] = QItem{ref[k], (int32_t)slot};
+#if GSX_GREEDY_BASE
+        const uint32_t q = atomicAdd(nout_p, 1u), slot = base + q;
+        (void)n4_p;
+#else
+        const uint32_t q = atomicAdd(nout_p, 1u), slot = atomicAdd(n4_p, 1u);
+        (void)base;
+#endif
+        qout[q] = QItem{ref[k], (int32_t)slot};
         ch[k] = (int32_t)slot;
       }
     }
@@ -298,12 +310,17 @@ __device__ inline void greedy_item(const float4* __restrict__ nodes, const QItem
 __global__ void k_greedy_level(const float4* __restrict__ nodes, QItem* qa, QItem* qb,
                                uint32_t* cnt, float4* __restrict__ nodes4, int level) {
   uint32_t* c = cnt + 3;
-  if (blockIdx.x == 0 && threadIdx.x == 0) c[(level + 2) % 3] = 0u;
+  uint32_t* b = cnt + 6;  // rotating level bases: b[L % 3] = slots used before level L's outputs
+  const uint32_t nin = c[level % 3];
+  const uint32_t base = b[(level + 2) % 3] + nin;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c[(level + 2) % 3] = 0u;
+    b[level % 3] = base;
+  }
   const QItem* qin = (level & 1) ? qb : qa;
   QItem* qout = (level & 1) ? qa : qb;
-  const uint32_t nin = c[level % 3];
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nin; i += gridDim.x * blockDim.x)
-    greedy_item(nodes, qin[i], qout, c + (level + 1) % 3, cnt + 2, nodes4);
+    greedy_item(nodes, qin[i], qout, c + (level + 1) % 3, cnt + 2, base, nodes4);
 }
 
 // The remaining levels from `first` on in one cooperative launch: a grid-wide
@@ -322,10 +339,15 @@ __global__ void k_greedy_all(const float4* __restrict__ nodes, QItem* qa, QItem*
     QItem* qout = (level & 1) ? qa : qb;
     uint32_t* cin = c + level % 3;
     uint32_t* cout = c + (level + 1) % 3;
-    if (grid.thread_rank() == 0) c[(level + 2) % 3] = 0u;
-    const uint32_t nin = *cin;
+    uint32_t* b = cnt + 6;
+    const uint32_t nin = *(volatile uint32_t*)cin;
+    const uint32_t base = *(volatile uint32_t*)(b + (level + 2) % 3) + nin;
+    if (grid.thread_rank() == 0) {
+      c[(level + 2) % 3] = 0u;
+      b[level % 3] = base;
+    }
     for (uint32_t i = (uint32_t)grid.thread_rank(); i < nin; i += (uint32_t)grid.size())
-      greedy_item(nodes, qin[i], qout, cout, cnt + 2, nodes4);
+      greedy_item(nodes, qin[i], qout, cout, cnt + 2, base, nodes4);
     grid.sync();
     if (*(volatile uint32_t*)cout == 0u) break;  // the same value for every thread
   }
@@ -339,6 +361,8 @@ __global__ void k_greedy_init(QItem* q, uint32_t* cnt) {
   cnt[3] = 1;  // k_greedy_all's rotating frontier sizes
   cnt[4] = 0;
   cnt[5] = 0;
+  cnt[6] = cnt[7] = 0;  // level bases (GSX_GREEDY_BASE): level 0's is b[2] + 1 = 1
+  cnt[8] = 0;
 }
 
 __global__ void k_export(const float4* nodes, int64_t m, float* boxes, int32_t* children) {
