@@ -440,7 +440,9 @@ __device__ bool backward_segment(const SceneView& sv, const BvhView& bv, const R
 //   P2: lobes 0-3 (7 rows each)                     -> batch (axes) / atomics
 //   P3: SH values 22-26 + lobes 4-6                 -> atomics / batch
 // An entry split by a 32-pair boundary contributes two batch rows; every
-// finished value is linear in them, so the atomics add up the same.
+// finished value is linear in them, so the atomics add up the same.  The
+// lobe rows are formed from terms the radiance evaluation keeps in registers
+// (radiance_lobe_terms), not from a second read of the appearance block.
 // ---------------------------------------------------------------------------
 constexpr int PR_ROW = 36;  // a row per lane, 32 pair columns (16-byte rows: float4 reads conflict-free)
 constexpr int PR_FLOATS = 32 * PR_ROW;
