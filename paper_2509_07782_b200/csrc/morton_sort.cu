@@ -3,7 +3,8 @@
 // spatial.py:92) and K4 permutation (Scene.apply_permutation, scene.py:74-80).
 //
 // Radix sort: 8 passes of 8 bits.  Each pass = per-tile digit histogram ->
-// device-wide exclusive scan of the digit-major histogram -> stable scatter.
+// device-wide exclusive scan of the digit-major histogram (per scan tile,
+// the scan tiles' totals added by the scatter) -> stable scatter.
 // Stability inside a tile comes from warp-level ranking (__match_any_sync)
 // over a contiguous 256-key sub-tile per warp, then an exclusive scan of the
 // per-warp digit counts.  All HBM-bound: per pass 2 reads + 1 write of
@@ -218,8 +219,8 @@ template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(SORT_THREADS)
     k_scatter(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
               int64_t n, int shift, int nblocks, const uint32_t* __restrict__ offsets,
-              uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
-              int64_t* __restrict__ perm_out) {
+              const uint32_t* __restrict__ tile_sums, uint64_t* __restrict__ keys_out,
+              int32_t* __restrict__ vals_out, int64_t* __restrict__ perm_out) {
   __shared__ uint32_t wcnt[SORT_WARPS][RADIX];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < SORT_WARPS * RADIX; k += SORT_THREADS) (&wcnt[0][0])[k] = 0;
@@ -263,7 +264,10 @@ __global__ void __launch_bounds__(SORT_THREADS)
     int64_t i = base + it * 32 + lane;
     if (i < n) {
       uint32_t d = dig[it];
-      uint32_t pos = offsets[(size_t)d * nblocks + blockIdx.x] + wcnt[w][d] + rank[it];
+      // offsets holds the scan within each SCAN_TILE of the histogram;
+      // tile_sums the scanned tile totals (k_scan_add folded in here)
+      const size_t hi = (size_t)d * nblocks + blockIdx.x;
+      uint32_t pos = offsets[hi] + tile_sums[hi / SCAN_TILE] + wcnt[w][d] + rank[it];
       keys_out[pos] = key[it];
       if (LAST)
         perm_out[pos] = (int64_t)val[it];
@@ -376,17 +380,16 @@ extern "C" int gsx_sort_codes(const uint64_t* keys_in, int64_t n, uint64_t* keys
     k_hist<<<nb, SORT_THREADS, 0, s>>>(ksrc, n, shift, nb, w.hist);
     k_scan_tiles<<<sb, SCAN_THREADS, 0, s>>>(w.hist, hl, w.sums);
     k_scan_sums<<<1, SCAN_THREADS, 0, s>>>(w.sums, sb);
-    k_scan_add<<<sb, SCAN_THREADS, 0, s>>>(w.hist, hl, w.sums);
     bool first = p == 0, last = p == passes - 1;
     if (first)
-      k_scatter<true, false><<<nb, SORT_THREADS, 0, s>>>(ksrc, vsrc, n, shift, nb, w.hist, kdst,
-                                                         vdst, nullptr);
+      k_scatter<true, false><<<nb, SORT_THREADS, 0, s>>>(
+          ksrc, vsrc, n, shift, nb, w.hist, w.sums, kdst, vdst, nullptr);
     else if (last)
-      k_scatter<false, true><<<nb, SORT_THREADS, 0, s>>>(ksrc, vsrc, n, shift, nb, w.hist, kdst,
-                                                         nullptr, perm_out);
+      k_scatter<false, true><<<nb, SORT_THREADS, 0, s>>>(
+          ksrc, vsrc, n, shift, nb, w.hist, w.sums, kdst, nullptr, perm_out);
     else
-      k_scatter<false, false><<<nb, SORT_THREADS, 0, s>>>(ksrc, vsrc, n, shift, nb, w.hist, kdst,
-                                                          vdst, nullptr);
+      k_scatter<false, false><<<nb, SORT_THREADS, 0, s>>>(
+          ksrc, vsrc, n, shift, nb, w.hist, w.sums, kdst, vdst, nullptr);
     ksrc = kdst;
     vsrc = vdst;
   }
