@@ -1,4 +1,4 @@
-for l in libgsx.so; do
+for l in libgsx.so libgsx_ei.so; do
   export GSX_LIB=$PWD/paper_2509_07782_b200/$l
   echo "== $l"
   python -m pytest tests/test_gpu_grad.py -x -q 2>&1 | tail -1
